@@ -1,0 +1,331 @@
+"""Benchmark of the B200 nodal-DG Maxwell operator (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[2], the metric's N=4 single-GPU config): PEC
+cubic cavity, box (55,55,55) -> 998,250 tets, order N=4, fp32, TM (1,1,1)
+cavity-mode initial state, dt = stable_dt(cfl=1).  A *step* is one LSRK4
+step = 5 launches of the fused stage kernel over all elements.  The state
+register (0.86 GB) and residual are far larger than the 126 MB L2, so no
+explicit flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--gpus N > 1 runs under torchrun, one rank per GPU (NCCL); see DESIGN.md.
+--impl reference times the reference algorithm (the numpy oracle port of
+simtdg's ReferenceMaxwellOperator.rhs + rk4_step) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Maxwell DG net GFLOP/s & DOF-updates/s per RK4 step (N=4, tets); HBM GB/s"
+UNIT = "GFLOP/s"
+ORDER = 4
+CELLS = (55, 55, 55)
+CPU_SAMPLE_CELLS = (6, 6, 7)
+
+
+def _peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+def _ncu_summary() -> dict:
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self) -> dict:
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_rate(order: int, cells, steps: int, warmup: int = 0):
+    """Time the oracle port (reference algorithm, single thread) on a bounded sample."""
+    import numpy as np
+
+    from oracle import build_oracle_operator, rk4_step
+    from paper_0901_1024_b200 import (CavityMode, build_reference_element, compute_geometry, generate_box_mesh,
+                                      map_nodes, stable_dt)
+    from paper_0901_1024_b200.perfmodel import flops_per_element_stage
+
+    mesh = generate_box_mesh((1.0, 1.0, 1.0), cells)
+    elem = build_reference_element(order)
+    ora = build_oracle_operator(mesh, elem)
+    u = CavityMode(1, 1, 1, (1.0, 1.0, 1.0)).evaluate(map_nodes(mesh, elem), 0.0)
+    dt = stable_dt(mesh, compute_geometry(mesh), order)
+    for _ in range(warmup):
+        u = rk4_step(u, 0.0, dt, lambda t, y: ora.rhs(y))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        u = rk4_step(u, 0.0, dt, lambda t, y: ora.rhs(y))
+    sec = time.perf_counter() - t0
+    k = mesh.num_elements
+    flops = flops_per_element_stage(order) * k * 5 * steps
+    dof = 6 * elem.num_nodes * k * steps
+    assert np.isfinite(u).all()
+    return {"gflops": flops / sec / 1e9, "dof_updates_per_s": dof / sec, "seconds": sec, "elements": k,
+            "steps": steps}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    r = cpu_reference_rate(ORDER, CPU_SAMPLE_CELLS, args.steps, args.warmup)
+    sample = (f"box {CPU_SAMPLE_CELLS} -> {r['elements']} tets, N={ORDER}, {args.steps} LSRK4 steps after "
+              f"{args.warmup} warm-up (the full {CELLS} workload needs ~44 GB and ~7 min per step on this path); "
+              "rate is per-DOF and nearly K-independent")
+    line = {
+        "metric": METRIC, "value": r["gflops"], "unit": UNIT, "impl": "reference", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "dof_updates_per_s": r["dof_updates_per_s"],
+        "config": {"workload": f"C3 Maxwell PEC cavity N={ORDER}, box {CELLS}", "order": ORDER,
+                   "sample_elements": r["elements"], "path": "oracle port of simtdg ReferenceMaxwellOperator.rhs "
+                   "+ rk4_step (numpy einsum, single-threaded as the reference)"},
+        "cpu_baseline": {"value": r["gflops"], "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": r["gflops"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args) -> None:
+    import numpy as np
+    import torch
+
+    from paper_0901_1024_b200 import (CavityMode, build_b200_operator, build_reference_element, compute_geometry,
+                                      generate_box_mesh, map_nodes, stable_dt)
+    from paper_0901_1024_b200.perfmodel import bytes_per_element_stage, dofs, flops_per_element_stage
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    dtype = torch.float64 if args.dtype == "f64" else torch.float32
+    word = 8 if dtype == torch.float64 else 4
+    cells = tuple(args.cells)
+    t_setup = time.perf_counter()
+    mesh = generate_box_mesh((1.0, 1.0, 1.0), cells)
+    elem = build_reference_element(args.order)
+    op = build_b200_operator(mesh, elem, dtype=dtype, device=dev)
+    geo = op.geometry
+    dt = stable_dt(mesh, geo, args.order)
+    u0_host = CavityMode(1, 1, 1, (1.0, 1.0, 1.0)).evaluate(map_nodes(mesh, elem), 0.0)
+    u = op.to_padded(u0_host)
+    setup_s = time.perf_counter() - t_setup
+    k = op.num_elements
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- device-resident throughput (value) ----
+    op.advance(u, dt, args.warmup, use_graph=False)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        op.advance(u, dt, args.steps, use_graph=False)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    energy = op.field_energy(u)
+    if not math.isfinite(energy):
+        raise RuntimeError("non-finite energy after the timed steps")
+
+    launches = 5 * args.steps
+    sec = ms / 1e3
+    f_alg = flops_per_element_stage(args.order)
+    b_alg = bytes_per_element_stage(args.order, word)
+    gflops = world * f_alg * k * 5 * args.steps / sec / 1e9
+    dof_rate = world * dofs(args.order, k) * args.steps / sec
+    hbm_gbs = b_alg * k * 5 * args.steps / sec / 1e9  # per GPU
+    launch_s = sec / launches
+    peaks = _peaks()
+    ncu = _ncu_summary()
+    traffic = ncu.get("stage_kernel", {}).get("dram_bytes_per_launch")
+    fp32_peak_tf = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+
+    # ---- end-to-end through the public API with host buffers ----
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    host_in = torch.from_numpy(np.ascontiguousarray(u0_host)).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    h2d = host_in.numel() * host_in.element_size()
+    d2h = host_out.numel() * host_out.element_size() + 8
+    # warm-up one e2e step
+    ue = op.to_padded(host_in.to(dev, non_blocking=True))
+    op.advance(ue, dt, 1, use_graph=False)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for _ in range(e2e_steps):
+        ue = op.to_padded(host_in.to(dev, non_blocking=True), out=ue)   # H2D + pack (f64 natural -> padded)
+        op.advance(ue, dt, 1, use_graph=False)                          # 5 fused stage launches
+        host_out.copy_(op.from_padded(ue), non_blocking=True)           # unpack + D2H of the new state
+        energy_t = op.mass_norm(ue, 1.0, 1.0)                           # per-step diagnostic, as run_cavity
+        e_val = energy_t.to("cpu", non_blocking=True)
+    e_stop.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e_ms = e_start.elapsed_time(e_stop)
+    if world > 1:
+        t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e_gflops = world * f_alg * k * 5 * e2e_steps / (e_ms / 1e3) / 1e9
+    del e_val
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_rate(args.order, CPU_SAMPLE_CELLS, args.cpu_steps)
+        cpu = {"value": r["gflops"], "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"oracle port of the reference path, box {CPU_SAMPLE_CELLS} -> {r['elements']} tets, "
+                         f"N={args.order}, {args.cpu_steps} LSRK4 steps, {r['seconds']:.1f} s single-threaded; "
+                         f"{r['dof_updates_per_s']:.3g} DOF-updates/s"}
+    clk = clocks.summary()
+    line = {
+        "metric": METRIC, "value": gflops, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if word == 8 else "f32", "data": "synthetic",
+        "dof_updates_per_s": dof_rate, "hbm_gbs_algorithmic": hbm_gbs,
+        "config": {"workload": f"C3 Maxwell PEC cavity N={args.order}, box {cells} -> {k} tets per GPU, "
+                               "TM(1,1,1) cavity mode, dt=stable_dt(cfl=1)",
+                   "order": args.order, "elements_per_gpu": k, "dofs_per_gpu": dofs(args.order, k),
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "no flush: state+residual registers (%.2f GB) >> 126 MB L2" % (
+                       2 * 6 * k * op.np_stride * word / 1e9),
+                   "setup_s": round(setup_s, 2), "flops_per_element_stage": f_alg,
+                   "bytes_per_element_stage": b_alg},
+        "roofline": {"bound": "hbm", "achieved": b_alg * k / launch_s / 1e9, "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": b_alg * k / launch_s / 1e9 / peaks["hbm_gbs"],
+                     "traffic": traffic, "kernel": f"dgm::stage_kernel<{args.order},{'float' if word == 4 else 'double'},1>",
+                     "launch_us": launch_s * 1e6,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "_fallback" not in peaks
+                     else "fallback 6.65 TB/s (B200_PROFILING.md)",
+                     "fp32_simt_frac": f_alg * k / launch_s / 1e12 / fp32_peak_tf,
+                     "fp32_simt_peak_tflops": fp32_peak_tf},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_gflops, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,
+                "path": "op.to_padded(pinned f64 natural state) -> op.advance(1 step) -> op.from_padded -> "
+                        "pinned host, + field-norm scalar D2H"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "energy_after": energy,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main(argv=None) -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--order", type=int, default=ORDER)
+    ap.add_argument("--cells", type=int, nargs=3, default=list(CELLS))
+    ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-steps", type=int, default=12)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

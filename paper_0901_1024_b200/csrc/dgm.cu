@@ -1,0 +1,333 @@
+// dgm.cu -- C ABI of libdgm.so (see include/dgm.h for the contract).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <type_traits>
+#include <utility>
+
+#include "../../include/dgm.h"
+#include "dgm_aux.cuh"
+#include "dgm_stage.cuh"
+
+#define DGM_ABI_VERSION 1
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(DGM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return DGM_OK;
+}
+
+// Calls fn(std::integral_constant<int, N>, T) for the runtime (order, dtype).
+template <typename Fn>
+int dispatch(int order, int dtype, Fn&& fn) {
+  if (dtype != DGM_F32 && dtype != DGM_F64)
+    return fail(DGM_ERR_UNSUPPORTED, "dtype %d not supported", dtype);
+#define DGM_CASE(n)                                                          \
+  case n:                                                                    \
+    return dtype == DGM_F32 ? fn(std::integral_constant<int, n>{}, float{}) \
+                            : fn(std::integral_constant<int, n>{}, double{});
+  switch (order) {
+    DGM_CASE(1) DGM_CASE(2) DGM_CASE(3) DGM_CASE(4) DGM_CASE(5)
+    DGM_CASE(6) DGM_CASE(7) DGM_CASE(8) DGM_CASE(9)
+    default:
+      return fail(DGM_ERR_UNSUPPORTED, "order %d not supported (1..9)", order);
+  }
+#undef DGM_CASE
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  const int64_t cap = 148 * 32;
+  return (int)(b < cap ? b : cap);
+}
+
+}  // namespace
+
+struct dgm_plan {
+  dgm_desc d;
+  size_t stage_smem;  // dynamic smem of the stage kernels
+};
+
+extern "C" {
+
+int32_t dgm_version(void) { return DGM_ABI_VERSION; }
+
+const char* dgm_last_error(void) { return g_err; }
+
+int dgm_layout(int32_t order, int32_t dtype, dgm_layout_info* out) {
+  if (!out) return fail(DGM_ERR_INVALID, "dgm_layout: null output");
+  return dispatch(order, dtype, [&](auto n, auto t) -> int {
+    using C = dgm::Cfg<decltype(n)::value, decltype(t)>;
+    out->order = order;
+    out->dtype = dtype;
+    out->num_nodes = C::NP;
+    out->num_face_nodes = C::NFP;
+    out->np_stride = C::NPG;
+    out->diff_chunks = C::NJC;
+    out->lift_chunks = C::NLC;
+    out->vec = C::VEC;
+    out->tile_elements = C::TE;
+    out->threads = C::THREADS;
+    out->smem_bytes_fixed = (int64_t)C::SMEM_FIXED;
+    return DGM_OK;
+  });
+}
+
+int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
+  g_err[0] = 0;
+  if (!desc || !out) return fail(DGM_ERR_INVALID, "dgm_plan_create: null argument");
+  const dgm_desc& d = *desc;
+  if (d.num_elements < 0 || d.field_stride < d.num_elements)
+    return fail(DGM_ERR_INVALID, "field_stride (%lld) must be >= num_elements (%lld) >= 0",
+                (long long)d.field_stride, (long long)d.num_elements);
+  if (d.field_stride >= (int64_t)1 << 31)
+    return fail(DGM_ERR_INVALID, "field_stride must fit int32 element ids");
+  if (!(d.permittivity > 0.0) || !(d.permeability > 0.0))
+    return fail(DGM_ERR_INVALID, "material constants must be positive");
+  if (d.num_codes < 0 || d.num_codes > 4096)
+    return fail(DGM_ERR_INVALID, "num_codes %d out of range", d.num_codes);
+  const void* ptrs[] = {d.diff_packed, d.lift_packed, d.geometry};
+  for (const void* p : ptrs)
+    if (!p || !aligned16(p)) return fail(DGM_ERR_INVALID, "operand pointers must be non-null and 16-byte aligned");
+  if (!d.neighbors || !d.codes || !d.face_nodes || (d.num_codes > 0 && !d.code_table))
+    return fail(DGM_ERR_INVALID, "connectivity pointers must be non-null");
+  size_t smem = 0;
+  int rc = dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    smem = C::SMEM_FIXED + (size_t)d.num_codes * C::NFP;
+    smem = (smem + 15) & ~size_t(15);
+    if (smem > 227 * 1024)
+      return fail(DGM_ERR_UNSUPPORTED, "stage kernel needs %zu bytes of shared memory", smem);
+    int r;
+    if ((r = cuda_check(cudaFuncSetAttribute(dgm::stage_kernel<N, T, dgm::MODE_RHS>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "cudaFuncSetAttribute")))
+      return r;
+    if ((r = cuda_check(cudaFuncSetAttribute(dgm::stage_kernel<N, T, dgm::MODE_LSRK>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "cudaFuncSetAttribute")))
+      return r;
+    if ((r = cuda_check(cudaFuncSetAttribute(dgm::stage_kernel<N, T, dgm::MODE_VOLUME>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "cudaFuncSetAttribute")))
+      return r;
+    if ((r = cuda_check(cudaFuncSetAttribute(dgm::stage_kernel<N, T, dgm::MODE_SURFACE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "cudaFuncSetAttribute")))
+      return r;
+    const size_t msmem = (size_t)6 * C::TE * C::NPG * sizeof(T);
+    if ((r = cuda_check(cudaFuncSetAttribute(dgm::mass_norm_kernel<N, T>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem),
+                        "cudaFuncSetAttribute")))
+      return r;
+    return DGM_OK;
+  });
+  if (rc) return rc;
+  dgm_plan* p = new (std::nothrow) dgm_plan;
+  if (!p) return fail(DGM_ERR_INVALID, "out of host memory");
+  p->d = d;
+  p->stage_smem = smem;
+  *out = p;
+  return DGM_OK;
+}
+
+int dgm_plan_destroy(dgm_plan* plan) {
+  delete plan;
+  return DGM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <int MODE>
+int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, void* out, double a,
+                 double b, double dt, int64_t e_begin, int64_t e_end, void* stream) {
+  if (!plan) return fail(DGM_ERR_INVALID, "null plan");
+  const dgm_desc& d = plan->d;
+  if (e_begin < 0 || e_end > d.num_elements || e_begin > e_end)
+    return fail(DGM_ERR_INVALID, "element range [%lld, %lld) outside [0, %lld)", (long long)e_begin,
+                (long long)e_end, (long long)d.num_elements);
+  if (!u || !aligned16(u)) return fail(DGM_ERR_INVALID, "state pointer must be non-null and 16-byte aligned");
+  if (MODE == dgm::MODE_LSRK) {
+    if (!u_out || !res || !aligned16(u_out) || !aligned16(res))
+      return fail(DGM_ERR_INVALID, "u_out/res must be non-null and 16-byte aligned");
+    if (u_out == u) return fail(DGM_ERR_INVALID, "u_out must differ from u_in (neighbors read u_in)");
+  } else if (!out || !aligned16(out)) {
+    return fail(DGM_ERR_INVALID, "output pointer must be non-null and 16-byte aligned");
+  }
+  if (e_end == e_begin) return DGM_OK;
+  return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    dgm::StageArgs<T> args;
+    args.u = static_cast<const T*>(u);
+    args.u_out = static_cast<T*>(u_out);
+    args.res = static_cast<T*>(res);
+    args.out = static_cast<T*>(out);
+    args.geo = static_cast<const T*>(d.geometry);
+    args.nbr = d.neighbors;
+    args.code = d.codes;
+    args.diff = static_cast<const T*>(d.diff_packed);
+    args.lift = static_cast<const T*>(d.lift_packed);
+    args.fmask = d.face_nodes;
+    args.ptab = d.code_table;
+    args.ncodes = d.num_codes;
+    args.kf = d.field_stride;
+    args.e_begin = e_begin;
+    args.e_end = e_end;
+    args.a = (T)a;
+    args.b = (T)b;
+    args.dt = (T)dt;
+    args.a_zero = (a == 0.0);
+    args.inv_eps = (T)(1.0 / d.permittivity);
+    args.inv_mu = (T)(1.0 / d.permeability);
+    const double z = std::sqrt(d.permeability / d.permittivity);
+    args.zp = (T)z;
+    args.yp = (T)(1.0 / z);
+    args.inv_2z = (T)(1.0 / (2.0 * z));
+    args.inv_2y = (T)(1.0 / (2.0 * (1.0 / z)));
+    const int64_t tiles = (e_end - e_begin + C::TE - 1) / C::TE;
+    dgm::stage_kernel<N, T, MODE><<<(unsigned)tiles, C::THREADS, plan->stage_smem,
+                                    static_cast<cudaStream_t>(stream)>>>(args);
+    return cuda_check(cudaGetLastError(), "stage_kernel launch");
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int dgm_rhs(const dgm_plan* plan, const void* u, void* out, int64_t e_begin, int64_t e_end, void* stream) {
+  return launch_stage<dgm::MODE_RHS>(plan, u, nullptr, nullptr, out, 0, 0, 0, e_begin, e_end, stream);
+}
+
+int dgm_lsrk_stage(const dgm_plan* plan, const void* u_in, void* u_out, void* res, double a, double b,
+                   double dt, int64_t e_begin, int64_t e_end, void* stream) {
+  return launch_stage<dgm::MODE_LSRK>(plan, u_in, u_out, res, nullptr, a, b, dt, e_begin, e_end, stream);
+}
+
+int dgm_volume(const dgm_plan* plan, const void* u, void* out, int64_t e_begin, int64_t e_end, void* stream) {
+  return launch_stage<dgm::MODE_VOLUME>(plan, u, nullptr, nullptr, out, 0, 0, 0, e_begin, e_end, stream);
+}
+
+int dgm_surface(const dgm_plan* plan, const void* u, void* out, int64_t e_begin, int64_t e_end, void* stream) {
+  return launch_stage<dgm::MODE_SURFACE>(plan, u, nullptr, nullptr, out, 0, 0, 0, e_begin, e_end, stream);
+}
+
+int dgm_mass_norm(const dgm_plan* plan, const void* u, const void* mass_packed, const void* det_j, double w_e,
+                  double w_h, double* out_f64, int64_t e_begin, int64_t e_end, void* stream) {
+  if (!plan) return fail(DGM_ERR_INVALID, "null plan");
+  const dgm_desc& d = plan->d;
+  if (!u || !mass_packed || !det_j || !out_f64 || !aligned16(u) || !aligned16(mass_packed))
+    return fail(DGM_ERR_INVALID, "dgm_mass_norm: null or misaligned pointer");
+  if (e_begin < 0 || e_end > d.num_elements || e_begin > e_end)
+    return fail(DGM_ERR_INVALID, "element range outside the plan");
+  if (e_end == e_begin) return DGM_OK;
+  return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    const int64_t tiles = (e_end - e_begin + C::TE - 1) / C::TE;
+    const size_t msmem = (size_t)6 * C::TE * C::NPG * sizeof(T);
+    dgm::mass_norm_kernel<N, T><<<(unsigned)tiles, C::THREADS, msmem, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const T*>(u), static_cast<const T*>(mass_packed), static_cast<const T*>(det_j),
+        d.field_stride, e_begin, e_end, w_e, w_h, out_f64);
+    return cuda_check(cudaGetLastError(), "mass_norm_kernel launch");
+  });
+}
+
+int dgm_pack(int32_t order, int32_t dtype, const double* natural, void* padded, int64_t num_elements,
+             int64_t field_stride, void* stream) {
+  if (!natural || !padded || num_elements < 0 || field_stride < num_elements)
+    return fail(DGM_ERR_INVALID, "dgm_pack: bad arguments");
+  if (num_elements == 0) return DGM_OK;
+  return dispatch(order, dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    dgm::pack_kernel<N, T><<<grid_for(6 * num_elements * C::NPG, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        natural, static_cast<T*>(padded), num_elements, field_stride);
+    return cuda_check(cudaGetLastError(), "pack_kernel launch");
+  });
+}
+
+int dgm_unpack(int32_t order, int32_t dtype, const void* padded, double* natural, int64_t num_elements,
+               int64_t field_stride, void* stream) {
+  if (!natural || !padded || num_elements < 0 || field_stride < num_elements)
+    return fail(DGM_ERR_INVALID, "dgm_unpack: bad arguments");
+  if (num_elements == 0) return DGM_OK;
+  return dispatch(order, dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    dgm::unpack_kernel<N, T><<<grid_for(6 * num_elements * C::NP, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const T*>(padded), natural, num_elements, field_stride);
+    return cuda_check(cudaGetLastError(), "unpack_kernel launch");
+  });
+}
+
+int dgm_halo_pack(const dgm_plan* plan, const void* u, const int32_t* elements, int64_t count, void* sendbuf,
+                  void* stream) {
+  if (!plan || !u || (count > 0 && (!elements || !sendbuf)) || count < 0)
+    return fail(DGM_ERR_INVALID, "dgm_halo_pack: bad arguments");
+  if (!aligned16(u) || (sendbuf && !aligned16(sendbuf)))
+    return fail(DGM_ERR_INVALID, "dgm_halo_pack: buffers must be 16-byte aligned");
+  if (count == 0) return DGM_OK;
+  const dgm_desc& d = plan->d;
+  return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    dgm::halo_pack_kernel<N, T><<<grid_for(count * 6 * (C::NPG / C::VEC), 256), 256, 0,
+                                  static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const T*>(u), elements, count, d.field_stride, static_cast<T*>(sendbuf));
+    return cuda_check(cudaGetLastError(), "halo_pack_kernel launch");
+  });
+}
+
+int dgm_halo_unpack(const dgm_plan* plan, const void* recvbuf, int64_t count, int64_t ghost_begin, void* u,
+                    void* stream) {
+  if (!plan || !u || count < 0 || (count > 0 && !recvbuf))
+    return fail(DGM_ERR_INVALID, "dgm_halo_unpack: bad arguments");
+  const dgm_desc& d = plan->d;
+  if (ghost_begin < 0 || ghost_begin + count > d.field_stride)
+    return fail(DGM_ERR_INVALID, "ghost range [%lld, %lld) exceeds field_stride %lld", (long long)ghost_begin,
+                (long long)(ghost_begin + count), (long long)d.field_stride);
+  if (!aligned16(u) || (recvbuf && !aligned16(recvbuf)))
+    return fail(DGM_ERR_INVALID, "dgm_halo_unpack: buffers must be 16-byte aligned");
+  if (count == 0) return DGM_OK;
+  return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    dgm::halo_unpack_kernel<N, T><<<grid_for(count * 6 * (C::NPG / C::VEC), 256), 256, 0,
+                                    static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const T*>(recvbuf), count, ghost_begin, d.field_stride, static_cast<T*>(u));
+    return cuda_check(cudaGetLastError(), "halo_unpack_kernel launch");
+  });
+}
+
+}  // extern "C"

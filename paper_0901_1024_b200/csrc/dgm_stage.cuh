@@ -1,0 +1,370 @@
+// dgm_stage.cuh -- fused nodal-DG Maxwell stage kernel (SIMT path, sm_100a).
+//
+// One CTA owns a tile of TE consecutive elements and does, in one pass over
+// HBM, everything ReferenceMaxwellOperator.rhs (oracle.py:60-94) and one
+// iteration of rk4_step (assemble.py:118-120) do for those elements:
+//
+//   P0  stage u[6][TE][NPG], geometry, neighbor codes and the small face tables
+//       into shared memory (coalesced 16-byte loads);
+//   P1  surface: for every (element, face, face node) gather u- from smem and
+//       u+ from smem (neighbor in tile) or L2 (neighbor elsewhere) through the
+//       compact (neighbor, code) map, apply the PEC mirror on walls
+//       (maxwell.py:117-132) and the upwind flux (maxwell.py:73-114), scale by
+//       the face Jacobian (oracle.py:84-85) -> s_fl[6][TE][NFS];
+//   P2  volume + lift: thread (i, g) owns node i of elements g, g+G, ...;
+//       D_r,D_s,D_t rows stream from L1/L2 as 16-byte chunks (read-only path),
+//       u rows are broadcast from smem, 18 derivatives per (element, node)
+//       accumulate in registers, then the geometric transform and curls
+//       (oracle.py:68-79), then LIFT * flux, * 1/J, combine, / eps,mu
+//       (oracle.py:86-93);
+//   P3  write-back through smem: RHS, or the low-storage RK update
+//       res = a res + dt rhs; u_out = u + b res, fully coalesced.
+//
+// Algorithmic traffic per element-stage: read u, res; write
+// u, res (4*6*Np words) + 26 geometry words + 8 connectivity words.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dgm {
+
+constexpr int GEO_WORDS = 26;
+
+__host__ __device__ constexpr int np_of(int n) { return (n + 1) * (n + 2) * (n + 3) / 6; }
+__host__ __device__ constexpr int nfp_of(int n) { return (n + 1) * (n + 2) / 2; }
+
+// Smallest m >= n whose row size is a 16-byte multiple with an odd number of
+// 16-byte chunks: rows of consecutive elements then start in distinct 16-byte
+// bank groups, so 8 lanes reading 8 elements' rows are conflict-free.
+__host__ __device__ constexpr int odd_chunk_pad(int n, int w) {
+  int m = n;
+  while ((m * w) % 16 != 0 || ((m * w / 16) % 2) == 0) ++m;
+  return m;
+}
+
+template <int N, typename T>
+struct Cfg {
+  static constexpr int NP = np_of(N);
+  static constexpr int NFP = nfp_of(N);
+  static constexpr int NF4 = 4 * NFP;
+  static constexpr int W = sizeof(T);
+  static constexpr int VEC = 16 / W;
+  static constexpr int NPG = odd_chunk_pad(NP, W);   // u row stride (HBM and smem)
+  static constexpr int NFS = odd_chunk_pad(NF4, W);  // flux / rhs row stride (smem)
+  static constexpr int NJC = (NP + VEC - 1) / VEC;   // 16-byte chunks of a D row
+  static constexpr int NLC = (NF4 + VEC - 1) / VEC;  // 16-byte chunks of a LIFT row
+  static constexpr int G = (N <= 5) ? 8 : (N <= 7 ? 4 : 2);  // element groups
+  static constexpr int E = (W == 4) ? 4 : 2;                 // elements per thread
+  static constexpr int TE = G * E;                           // elements per tile
+  static constexpr int WORK = NP * G;
+  static constexpr int THREADS = ((WORK + 31) / 32) * 32;
+  static_assert(NF4 >= NP, "rhs rows reuse the flux buffer");
+  static constexpr size_t SMEM_REAL = (size_t)6 * TE * NPG + (size_t)6 * TE * NFS + (size_t)TE * GEO_WORDS;
+  static constexpr size_t SMEM_FIXED = SMEM_REAL * W + (size_t)TE * 8 * 4 + 4 * NFP;
+};
+
+template <typename T> struct V16;
+template <> struct V16<float> {
+  using type = float4;
+  __device__ static float dot(const float4& a, const float4& b) {
+    return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w)));
+  }
+};
+template <> struct V16<double> {
+  using type = double2;
+  __device__ static double dot(const double2& a, const double2& b) {
+    return fma(a.x, b.x, a.y * b.y);
+  }
+};
+
+template <typename T>
+struct StageArgs {
+  const T* u;          // (6, kf, NPG) input state
+  T* u_out;            // LSRK: updated state
+  T* res;              // LSRK: residual register
+  T* out;              // RHS / VOLUME: (6, kf, NPG); SURFACE: (6, kf, NF4)
+  const T* geo;        // (K, 26)
+  const int* nbr;      // (kf, 4)
+  const int* code;     // (kf, 4)
+  const T* diff;       // [3][NJC][NP][VEC]
+  const T* lift;       // [NLC][NP][VEC]
+  const uint8_t* fmask;  // [4][NFP]
+  const uint8_t* ptab;   // [ncodes][NFP]
+  int ncodes;
+  int64_t kf;          // field stride (element slots per field)
+  int64_t e_begin, e_end;
+  T a, b, dt;
+  T inv_eps, inv_mu;
+  T zp, yp;            // impedance / admittance of the (uniform) material
+  T inv_2z, inv_2y;    // 1 / (2 {Z}), 1 / (2 {Y})
+  int a_zero;          // LSRK: skip reading res (RK_A[0] == 0)
+};
+
+enum Mode { MODE_RHS = 0, MODE_LSRK = 1, MODE_VOLUME = 2, MODE_SURFACE = 3 };
+
+// Upwind flux difference (maxwell.py:73-114) for a uniform material.
+template <typename T>
+__device__ __forceinline__ void upwind(const T* um, const T* up, T nx, T ny, T nz,
+                                       const StageArgs<T>& a, T* out) {
+  const T dex = up[0] - um[0], dey = up[1] - um[1], dez = up[2] - um[2];
+  const T dhx = up[3] - um[3], dhy = up[4] - um[4], dhz = up[5] - um[5];
+  // n x [[E]], n x [[H]]
+  const T cex = ny * dez - nz * dey, cey = nz * dex - nx * dez, cez = nx * dey - ny * dex;
+  const T chx = ny * dhz - nz * dhy, chy = nz * dhx - nx * dhz, chz = nx * dhy - ny * dhx;
+  // E part: n x (Z+ [[H]] - n x [[E]]) / (2{Z})
+  const T ax = a.zp * dhx - cex, ay = a.zp * dhy - cey, az = a.zp * dhz - cez;
+  out[0] = (ny * az - nz * ay) * a.inv_2z;
+  out[1] = (nz * ax - nx * az) * a.inv_2z;
+  out[2] = (nx * ay - ny * ax) * a.inv_2z;
+  // H part: n x (-Y+ [[E]] - n x [[H]]) / (2{Y})
+  const T bx = -a.yp * dex - chx, by = -a.yp * dey - chy, bz = -a.yp * dez - chz;
+  out[3] = (ny * bz - nz * by) * a.inv_2y;
+  out[4] = (nz * bx - nx * bz) * a.inv_2y;
+  out[5] = (nx * by - ny * bx) * a.inv_2y;
+}
+
+template <int N, typename T, int MODE>
+__global__ void __launch_bounds__(Cfg<N, T>::THREADS)
+stage_kernel(const StageArgs<T> a) {
+  using C = Cfg<N, T>;
+  using V = typename V16<T>::type;
+  constexpr int TE = C::TE, NPG = C::NPG, NFS = C::NFS, NP = C::NP, NFP = C::NFP;
+  constexpr int VEC = C::VEC, G = C::G, E = C::E;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* s_u = reinterpret_cast<T*>(smem_raw);
+  T* s_fl = s_u + 6 * TE * NPG;
+  T* s_geo = s_fl + 6 * TE * NFS;
+  int* s_nbr = reinterpret_cast<int*>(s_geo + TE * GEO_WORDS);
+  int* s_code = s_nbr + TE * 4;
+  uint8_t* s_fmask = reinterpret_cast<uint8_t*>(s_code + TE * 4);
+  uint8_t* s_ptab = s_fmask + 4 * NFP;
+
+  const int tid = threadIdx.x;
+  const int64_t e0 = a.e_begin + (int64_t)blockIdx.x * TE;
+  const int nv = (int)min((int64_t)TE, a.e_end - e0);
+  const int64_t fstride = a.kf * NPG;
+
+  // ---------------- P0: stage the tile ----------------
+  {
+    constexpr int RV = NPG / VEC;  // 16-byte chunks per u row
+    const int nvec = nv * RV;
+    const V* src = reinterpret_cast<const V*>(a.u + e0 * NPG);
+    V* dst = reinterpret_cast<V*>(s_u);
+    const V zero = {};
+#pragma unroll 1
+    for (int f = 0; f < 6; ++f) {
+      const V* sf = src + (size_t)f * (fstride / VEC);
+      V* df = dst + f * TE * RV;
+      for (int c = tid; c < TE * RV; c += blockDim.x) df[c] = (c < nvec) ? sf[c] : zero;
+    }
+    const T* gsrc = a.geo + e0 * GEO_WORDS;
+    for (int c = tid; c < TE * GEO_WORDS; c += blockDim.x)
+      s_geo[c] = (c < nv * GEO_WORDS) ? gsrc[c] : T(0);
+    if (MODE != MODE_VOLUME) {
+      for (int c = tid; c < nv * 4; c += blockDim.x) {
+        s_nbr[c] = a.nbr[e0 * 4 + c];
+        s_code[c] = a.code[e0 * 4 + c];
+      }
+      for (int c = tid; c < 4 * NFP; c += blockDim.x) s_fmask[c] = a.fmask[c];
+      for (int c = tid; c < a.ncodes * NFP; c += blockDim.x) s_ptab[c] = a.ptab[c];
+    }
+  }
+  __syncthreads();
+
+  // ---------------- P1: surface flux ----------------
+  if (MODE != MODE_VOLUME) {
+    const int nwork = nv * 4 * NFP;
+    for (int w = tid; w < nwork; w += blockDim.x) {
+      const int k = w / (4 * NFP);
+      const int r = w - k * (4 * NFP);
+      const int face = r / NFP;
+      const int node = r - face * NFP;
+      const int im = s_fmask[face * NFP + node];
+      T um[6], up[6];
+#pragma unroll
+      for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + k) * NPG + im];
+      const T* gk = s_geo + k * GEO_WORDS;
+      const T nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
+      const int code = s_code[k * 4 + face];
+      if (code < 0) {
+        // PEC mirror (maxwell.py:117-132)
+        const T nde = nx * um[0] + ny * um[1] + nz * um[2];
+        const T ndh = nx * um[3] + ny * um[4] + nz * um[5];
+        up[0] = -um[0] + T(2) * nde * nx;
+        up[1] = -um[1] + T(2) * nde * ny;
+        up[2] = -um[2] + T(2) * nde * nz;
+        up[3] = um[3] - T(2) * ndh * nx;
+        up[4] = um[4] - T(2) * ndh * ny;
+        up[5] = um[5] - T(2) * ndh * nz;
+      } else {
+        const int nb = s_nbr[k * 4 + face];
+        const int jn = s_ptab[code * NFP + node];
+        const int64_t loc = (int64_t)nb - e0;
+        if (loc >= 0 && loc < nv) {
+#pragma unroll
+          for (int f = 0; f < 6; ++f) up[f] = s_u[(f * TE + (int)loc) * NPG + jn];
+        } else {
+          const T* p = a.u + (int64_t)nb * NPG + jn;
+#pragma unroll
+          for (int f = 0; f < 6; ++f) up[f] = __ldg(p + f * fstride);
+        }
+      }
+      T fl[6];
+      upwind(um, up, nx, ny, nz, a, fl);
+      const T sj = gk[22 + face];
+#pragma unroll
+      for (int f = 0; f < 6; ++f) s_fl[(f * TE + k) * NFS + r] = fl[f] * sj;
+    }
+    __syncthreads();
+  }
+
+  if (MODE == MODE_SURFACE) {
+    // bracket * face_jacobian, natural face layout (6, kf, 4 Nfp)
+    constexpr int NF4 = C::NF4;
+    for (int f = 0; f < 6; ++f)
+      for (int c = tid; c < nv * NF4; c += blockDim.x) {
+        const int k = c / NF4, j = c - k * NF4;
+        a.out[((int64_t)f * a.kf + e0 + k) * NF4 + j] = s_fl[(f * TE + k) * NFS + j];
+      }
+    return;
+  }
+
+  // ---------------- P2: volume + lift ----------------
+  T rhs[6][E];
+  const bool worker = tid < C::WORK;
+  const int i = tid / G;
+  const int g = tid - i * G;
+  if (worker) {
+    T acc[3][6][E];
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+#pragma unroll
+      for (int f = 0; f < 6; ++f)
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[m][f][e] = T(0);
+
+    const V* dv = reinterpret_cast<const V*>(a.diff);
+#pragma unroll 1
+    for (int jc = 0; jc < C::NJC; ++jc) {
+      V d[3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) d[m] = __ldg(dv + ((size_t)m * C::NJC + jc) * NP + i);
+#pragma unroll
+      for (int f = 0; f < 6; ++f)
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const V uv = *reinterpret_cast<const V*>(s_u + (f * TE + e * G + g) * NPG + jc * VEC);
+#pragma unroll
+          for (int m = 0; m < 3; ++m) acc[m][f][e] += V16<T>::dot(d[m], uv);
+        }
+    }
+    // geometric transform + curls (oracle.py:69-79)
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const T* gk = s_geo + (e * G + g) * GEO_WORDS;
+      T rx[3][3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m)
+#pragma unroll
+        for (int n = 0; n < 3; ++n) rx[m][n] = gk[m * 3 + n];
+      // grad[n][f] = sum_m rx[m][n] * acc[m][f]
+      auto grad = [&](int n, int f) {
+        return rx[0][n] * acc[0][f][e] + rx[1][n] * acc[1][f][e] + rx[2][n] * acc[2][f][e];
+      };
+      // curl E = (dy Ez - dz Ey, dz Ex - dx Ez, dx Ey - dy Ex); same for H
+      const T ce0 = grad(1, 2) - grad(2, 1), ce1 = grad(2, 0) - grad(0, 2), ce2 = grad(0, 1) - grad(1, 0);
+      const T ch0 = grad(1, 5) - grad(2, 4), ch1 = grad(2, 3) - grad(0, 5), ch2 = grad(0, 4) - grad(1, 3);
+      rhs[0][e] = ch0; rhs[1][e] = ch1; rhs[2][e] = ch2;
+      rhs[3][e] = -ce0; rhs[4][e] = -ce1; rhs[5][e] = -ce2;
+    }
+    if (MODE != MODE_VOLUME) {
+      T accl[6][E];
+#pragma unroll
+      for (int f = 0; f < 6; ++f)
+#pragma unroll
+        for (int e = 0; e < E; ++e) accl[f][e] = T(0);
+      const V* lv = reinterpret_cast<const V*>(a.lift);
+#pragma unroll 2
+      for (int jc = 0; jc < C::NLC; ++jc) {
+        const V l = __ldg(lv + (size_t)jc * NP + i);
+#pragma unroll
+        for (int f = 0; f < 6; ++f)
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const V fv = *reinterpret_cast<const V*>(s_fl + (f * TE + e * G + g) * NFS + jc * VEC);
+            accl[f][e] += V16<T>::dot(l, fv);
+          }
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const T inv_j = s_geo[(e * G + g) * GEO_WORDS + 9];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) rhs[f][e] += accl[f][e] * inv_j;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+#pragma unroll
+      for (int f = 0; f < 3; ++f) rhs[f][e] *= a.inv_eps;
+#pragma unroll
+      for (int f = 3; f < 6; ++f) rhs[f][e] *= a.inv_mu;
+    }
+  }
+  if (MODE != MODE_VOLUME) __syncthreads();  // every lift read of s_fl is done
+  if (worker) {
+#pragma unroll
+    for (int f = 0; f < 6; ++f)
+#pragma unroll
+      for (int e = 0; e < E; ++e) s_fl[(f * TE + e * G + g) * NFS + i] = rhs[f][e];
+  }
+  __syncthreads();
+
+  // ---------------- P3: coalesced write-back ----------------
+  {
+    constexpr int RV = NPG / VEC;
+    const int nvec = nv * RV;
+#pragma unroll 1
+    for (int f = 0; f < 6; ++f) {
+      const int64_t gbase = ((int64_t)f * a.kf + e0) * NPG;
+      for (int c = tid; c < nvec; c += blockDim.x) {
+        const int k = c / RV, jv = c - k * RV;
+        T rh[VEC];
+        const T* srow = s_fl + (f * TE + k) * NFS + jv * VEC;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) rh[q] = (jv * VEC + q < NP) ? srow[q] : T(0);
+        const int64_t go = gbase + (int64_t)c * VEC;  // rows are contiguous: k*NPG + jv*VEC
+        if (MODE == MODE_RHS || MODE == MODE_VOLUME) {
+          V o;
+          T* op = reinterpret_cast<T*>(&o);
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) op[q] = rh[q];
+          *reinterpret_cast<V*>(a.out + go) = o;
+        } else {
+          V r;
+          T* rp = reinterpret_cast<T*>(&r);
+          if (a.a_zero) {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) rp[q] = a.dt * rh[q];
+          } else {
+            const V ro = *reinterpret_cast<const V*>(a.res + go);
+            const T* rop = reinterpret_cast<const T*>(&ro);
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) rp[q] = a.a * rop[q] + a.dt * rh[q];
+          }
+          *reinterpret_cast<V*>(a.res + go) = r;
+          const V uo = *reinterpret_cast<const V*>(s_u + (f * TE + k) * NPG + jv * VEC);
+          const T* uop = reinterpret_cast<const T*>(&uo);
+          V un;
+          T* unp = reinterpret_cast<T*>(&un);
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) unp[q] = uop[q] + a.b * rp[q];
+          *reinterpret_cast<V*>(a.u_out + go) = un;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace dgm

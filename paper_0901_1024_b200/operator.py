@@ -1,0 +1,368 @@
+"""The B200 Maxwell DG operator: drop-in for ``ReferenceMaxwellOperator``.
+
+``build_b200_operator(mesh, elem, material)`` takes the same ``Mesh`` and
+``ReferenceElement`` objects as the reference's ``build_reference_operator``
+(oracle.py:97-141) and returns an operator whose ``rhs(state)`` has the same
+contract (natural (6, K, Np) in, new array out, numpy stays numpy), plus the
+device-resident fast path:
+
+* ``to_padded`` / ``from_padded``: natural <-> element-aligned, zero-padded,
+  field-major device layout (6, field_stride, np_stride) (fields.py:24-35);
+* ``rhs_padded(u)``: one launch of the fused stage kernel in RHS mode;
+* ``advance(u, dt, n)``: n LSRK4 steps, each 5 launches of the fused
+  LIFT+RK stage kernel (RK_A/RK_B as assemble.py:80-114), CUDA-graph captured;
+* ``field_energy`` / ``l2_error``: device reductions (maxwell.py:211-232).
+
+All device memory is owned by torch tensors; the C library borrows pointers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _capi
+from .facemaps import FaceMaps, build_face_maps
+from .maxwell import VACUUM, Material
+from .mesh import FaceConnectivity, GeometricFactors, Mesh, build_connectivity, compute_geometry, map_nodes
+from .refelem import NUM_FACES, ReferenceElement
+from .stepper import RK_A, RK_B, RK_C
+
+N_FIELDS = 6
+_DTYPES = {torch.float32: _capi.DGM_F32, torch.float64: _capi.DGM_F64}
+
+
+def pack_chunks(mat: np.ndarray, chunks: int, vec: int) -> np.ndarray:
+    """(rows, cols) -> (chunks, rows, vec) with packed[c, i, q] = mat[i, c*vec + q] (0 past cols)."""
+    rows, cols = mat.shape
+    padded = np.zeros((rows, chunks * vec))
+    padded[:, :cols] = mat
+    return np.ascontiguousarray(padded.reshape(rows, chunks, vec).transpose(1, 0, 2))
+
+
+def geometry_words(geometry: GeometricFactors) -> np.ndarray:
+    """(K, 26) float64 per-element words, layout of dgm_desc.geometry (include/dgm.h)."""
+    k = len(geometry.det_jacobians)
+    g = np.empty((k, _capi.GEO_WORDS))
+    g[:, 0:9] = geometry.inv_jacobians.reshape(k, 9)
+    g[:, 9] = 1.0 / geometry.det_jacobians
+    g[:, 10:22] = geometry.normals.reshape(k, 12)
+    g[:, 22:26] = geometry.face_jacobians
+    return g
+
+
+@dataclass
+class _Buffers:
+    alt: torch.Tensor
+    res: torch.Tensor
+
+
+class B200MaxwellOperator:
+    """Maxwell RHS and LSRK4 on one B200 (or one rank's element range)."""
+
+    def __init__(self, elem: ReferenceElement, material: Material, geo_words: np.ndarray,
+                 det_j: np.ndarray, maps: FaceMaps, *, num_ghost: int = 0,
+                 dtype: torch.dtype = torch.float32, device=None):
+        if dtype not in _DTYPES:
+            raise ValueError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
+        if not torch.cuda.is_available():
+            raise RuntimeError("B200MaxwellOperator needs a CUDA device (no CPU fallback)")
+        self.elem = elem
+        self.material = material
+        self.dtype = dtype
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.num_elements = int(len(det_j))
+        self.num_ghost = int(num_ghost)
+        self.field_stride = self.num_elements + self.num_ghost
+        self._dt_code = _DTYPES[dtype]
+        self.layout = _capi.layout(elem.order, self._dt_code)
+        lay = self.layout
+        self.np_stride = lay.np_stride
+        self.maps = maps
+
+        def dev(a, dt=dtype):
+            return torch.as_tensor(np.ascontiguousarray(a)).to(device=self.device, dtype=dt)
+
+        self._diff = dev(np.stack([pack_chunks(elem.diff[m], lay.diff_chunks, lay.vec) for m in range(3)]))
+        self._lift = dev(pack_chunks(elem.lift, lay.lift_chunks, lay.vec))
+        self._mass = dev(pack_chunks(elem.mass, lay.diff_chunks, lay.vec))
+        self._geo = dev(geo_words)
+        self._det = dev(det_j)
+        nbr = np.zeros((self.field_stride, NUM_FACES), dtype=np.int32)
+        cod = np.full((self.field_stride, NUM_FACES), -1, dtype=np.int32)
+        nbr[: self.num_elements] = maps.neighbors
+        cod[: self.num_elements] = maps.codes
+        self._nbr = dev(nbr, torch.int32)
+        self._code = dev(cod, torch.int32)
+        self._fmask = dev(np.asarray(elem.face_nodes, dtype=np.uint8), torch.uint8)
+        table = maps.code_table if len(maps.code_table) else np.zeros((1, elem.num_face_nodes), np.uint8)
+        self._ptab = dev(table, torch.uint8)
+        self._num_codes = int(len(maps.code_table))
+
+        desc = _capi.Desc(
+            order=elem.order, dtype=self._dt_code, num_elements=self.num_elements,
+            field_stride=self.field_stride,
+            diff_packed=self._diff.data_ptr(), lift_packed=self._lift.data_ptr(),
+            geometry=self._geo.data_ptr(), neighbors=self._nbr.data_ptr(),
+            codes=self._code.data_ptr(), face_nodes=self._fmask.data_ptr(),
+            code_table=self._ptab.data_ptr(), num_codes=self._num_codes,
+            permittivity=float(material.permittivity), permeability=float(material.permeability))
+        lib = _capi.load()
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _capi.check(lib.dgm_plan_create(ctypes.byref(desc), ctypes.byref(handle)), "dgm_plan_create")
+        self._plan = handle
+        self._lib = lib
+        self._bufs: _Buffers | None = None
+        self._graphs: dict = {}
+        self._norm_out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        # reference-operator attributes, filled by build_b200_operator
+        self.mesh: Mesh | None = None
+        self.connectivity: FaceConnectivity | None = None
+        self.geometry: GeometricFactors | None = None
+        self._nodes = None
+
+    def __del__(self):
+        plan = getattr(self, "_plan", None)
+        if plan is not None and plan.value and _capi._lib is not None:
+            _capi._lib.dgm_plan_destroy(plan)
+            self._plan = None
+
+    # ------------------------------------------------------------------ info
+    @property
+    def order(self) -> int:
+        return self.elem.order
+
+    @property
+    def dofs(self) -> int:
+        """Degrees of freedom 6 * Np * K of the owned elements."""
+        return N_FIELDS * self.elem.num_nodes * self.num_elements
+
+    @property
+    def nodes(self) -> np.ndarray:
+        if self._nodes is None:
+            self._nodes = map_nodes(self.mesh, self.elem)
+        return self._nodes
+
+    @property
+    def vmap_minus(self) -> np.ndarray:
+        return self.maps.vmap_minus
+
+    @property
+    def vmap_plus(self) -> np.ndarray:
+        return self.maps.vmap_plus
+
+    @property
+    def is_boundary(self) -> np.ndarray:
+        return self.maps.is_boundary
+
+    @property
+    def normals(self) -> np.ndarray:
+        return self.geometry.normals
+
+    @property
+    def face_areas_global(self) -> np.ndarray:
+        from .refelem import FACE_AREAS
+
+        return self.geometry.face_jacobians * FACE_AREAS
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    # ---------------------------------------------------------------- layout
+    def empty_state(self) -> torch.Tensor:
+        """Zeroed padded state (6, field_stride, np_stride) on the device."""
+        return torch.zeros((N_FIELDS, self.field_stride, self.np_stride), dtype=self.dtype, device=self.device)
+
+    def _check_padded(self, u: torch.Tensor, name: str = "state") -> None:
+        if not isinstance(u, torch.Tensor):
+            raise TypeError(f"{name} must be a torch tensor in the padded device layout")
+        want = (N_FIELDS, self.field_stride, self.np_stride)
+        if tuple(u.shape) != want:
+            raise ValueError(f"{name} has shape {tuple(u.shape)}, expected padded {want}")
+        if u.dtype != self.dtype or u.device != self.device or not u.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous {self.dtype} tensor on {self.device}")
+
+    def to_padded(self, natural, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Natural (6, K, Np) numpy/torch -> padded device tensor (padding zero)."""
+        k, n_p = self.num_elements, self.elem.num_nodes
+        src = torch.as_tensor(natural)
+        if tuple(src.shape) != (N_FIELDS, k, n_p):
+            raise ValueError(f"natural state must have shape (6, {k}, {n_p}), got {tuple(src.shape)}")
+        src = src.to(device=self.device, dtype=torch.float64).contiguous()
+        if out is None:
+            out = self.empty_state()
+        else:
+            self._check_padded(out, "out")
+        _capi.check(self._lib.dgm_pack(self.order, self._dt_code, src.data_ptr(), out.data_ptr(), k,
+                                       self.field_stride, self._stream()), "dgm_pack")
+        return out
+
+    def from_padded(self, padded: torch.Tensor) -> torch.Tensor:
+        """Padded device tensor -> natural (6, K, Np) float64 device tensor."""
+        self._check_padded(padded, "padded")
+        out = torch.empty((N_FIELDS, self.num_elements, self.elem.num_nodes), dtype=torch.float64,
+                          device=self.device)
+        _capi.check(self._lib.dgm_unpack(self.order, self._dt_code, padded.data_ptr(), out.data_ptr(),
+                                         self.num_elements, self.field_stride, self._stream()), "dgm_unpack")
+        return out
+
+    def check_padding(self, padded: torch.Tensor) -> bool:
+        """True when every padding slot is exactly zero (fields.py:55-58)."""
+        return bool((padded[:, : self.num_elements, self.elem.num_nodes:] == 0).all().item())
+
+    # ------------------------------------------------------------- operators
+    def _range(self, e_begin, e_end):
+        e_begin = 0 if e_begin is None else int(e_begin)
+        e_end = self.num_elements if e_end is None else int(e_end)
+        return e_begin, e_end
+
+    def rhs_padded(self, u: torch.Tensor, out: torch.Tensor | None = None,
+                   e_begin=None, e_end=None) -> torch.Tensor:
+        """Fused RHS in the device layout (one kernel launch)."""
+        self._check_padded(u)
+        if out is None:
+            out = torch.zeros_like(u)
+        else:
+            self._check_padded(out, "out")
+        b, e = self._range(e_begin, e_end)
+        _capi.check(self._lib.dgm_rhs(self._plan, u.data_ptr(), out.data_ptr(), b, e, self._stream()), "dgm_rhs")
+        return out
+
+    def volume_padded(self, u: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Volume term only, (curl H/eps, -curl E/mu) (oracle.py:67-79)."""
+        self._check_padded(u)
+        out = torch.zeros_like(u) if out is None else out
+        _capi.check(self._lib.dgm_volume(self._plan, u.data_ptr(), out.data_ptr(), 0, self.num_elements,
+                                         self._stream()), "dgm_volume")
+        return out
+
+    def surface_flux(self, u: torch.Tensor) -> torch.Tensor:
+        """upwind_flux * face_jacobian per face node, (6, K, 4*Nfp) (oracle.py:82-85)."""
+        self._check_padded(u)
+        nf4 = NUM_FACES * self.elem.num_face_nodes
+        out = torch.zeros((N_FIELDS, self.field_stride, nf4), dtype=self.dtype, device=self.device)
+        _capi.check(self._lib.dgm_surface(self._plan, u.data_ptr(), out.data_ptr(), 0, self.num_elements,
+                                          self._stream()), "dgm_surface")
+        return out[:, : self.num_elements]
+
+    def rhs(self, state):
+        """Reference-compatible RHS: natural (6, K, Np) in, new array of the same kind out."""
+        is_numpy = not isinstance(state, torch.Tensor)
+        u = self.to_padded(state)
+        out = self.from_padded(self.rhs_padded(u))
+        if is_numpy:
+            return out.cpu().numpy()
+        return out.to(device=state.device)
+
+    rhs_natural = rhs
+
+    def lsrk_stage(self, u_in: torch.Tensor, u_out: torch.Tensor, res: torch.Tensor, a: float, b: float,
+                   dt: float, e_begin=None, e_end=None) -> None:
+        """res = a res + dt rhs(u_in); u_out = u_in + b res  (one fused launch)."""
+        bb, ee = self._range(e_begin, e_end)
+        _capi.check(self._lib.dgm_lsrk_stage(self._plan, u_in.data_ptr(), u_out.data_ptr(), res.data_ptr(),
+                                             float(a), float(b), float(dt), bb, ee, self._stream()),
+                    "dgm_lsrk_stage")
+
+    def _buffers(self) -> _Buffers:
+        if self._bufs is None:
+            self._bufs = _Buffers(alt=self.empty_state(), res=self.empty_state())
+        return self._bufs
+
+    def _launch_steps(self, u: torch.Tensor, dt: float, nsteps: int) -> torch.Tensor:
+        """nsteps LSRK4 steps ping-ponging u <-> alt; returns the tensor holding the result."""
+        bufs = self._buffers()
+        cur, nxt = u, bufs.alt
+        for _ in range(nsteps):
+            for a, b in zip(RK_A, RK_B):
+                self.lsrk_stage(cur, nxt, bufs.res, a, b, dt)
+                cur, nxt = nxt, cur
+        return cur
+
+    def advance(self, u: torch.Tensor, dt: float, nsteps: int = 1, use_graph: bool | None = None) -> torch.Tensor:
+        """Advance the padded state in place by nsteps LSRK4 steps of size dt."""
+        self._check_padded(u)
+        if dt <= 0.0:
+            raise ValueError("dt must be positive")
+        nsteps = int(nsteps)
+        if nsteps < 0:
+            raise ValueError("nsteps must be >= 0")
+        if nsteps == 0:
+            return u
+        if use_graph is None:
+            use_graph = nsteps >= 4
+        if not use_graph:
+            cur = self._launch_steps(u, dt, nsteps)
+            if cur is not u:
+                u.copy_(cur)
+            return u
+        pairs, odd = divmod(nsteps, 2)
+        if pairs:
+            graph = self._graph_for(u, dt)
+            for _ in range(pairs):
+                graph.replay()
+        if odd:
+            cur = self._launch_steps(u, dt, 1)
+            u.copy_(cur)
+        return u
+
+    def _graph_for(self, u: torch.Tensor, dt: float):
+        """CUDA graph of two LSRK4 steps (10 stage launches, u -> alt -> ... -> u)."""
+        key = (u.data_ptr(), float(dt))
+        graph = self._graphs.get(key)
+        if graph is None:
+            bufs = self._buffers()
+            # load the stage kernel outside capture (scratch buffers only)
+            self.lsrk_stage(u, bufs.alt, bufs.res, 0.0, 0.0, 0.0, 0, min(self.num_elements, 1))
+            torch.cuda.current_stream(self.device).synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                cur = self._launch_steps(u, dt, 2)
+                assert cur is u
+            self._graphs[key] = graph
+        return graph
+
+    def step(self, u: torch.Tensor, dt: float) -> torch.Tensor:
+        """One LSRK4 step in place (5 fused stage launches)."""
+        return self.advance(u, dt, 1, use_graph=False)
+
+    # ---------------------------------------------------------- diagnostics
+    def mass_norm(self, u: torch.Tensor, w_e: float = 1.0, w_h: float = 1.0) -> torch.Tensor:
+        """Device scalar sum_k J_k sum_f w_f u^T M u (float64 tensor, no sync)."""
+        self._check_padded(u)
+        out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        _capi.check(self._lib.dgm_mass_norm(self._plan, u.data_ptr(), self._mass.data_ptr(), self._det.data_ptr(),
+                                            float(w_e), float(w_h), out.data_ptr(), 0, self.num_elements,
+                                            self._stream()), "dgm_mass_norm")
+        return out
+
+    def field_energy(self, u: torch.Tensor) -> float:
+        """1/2 (eps |E|^2 + mu |H|^2) (maxwell.py:225-232)."""
+        m = self.material
+        return 0.5 * float(self.mass_norm(u, m.permittivity, m.permeability).item())
+
+    def l2_error(self, u: torch.Tensor, mode, t: float) -> float:
+        """Mass-weighted L2 distance to ``mode`` at time t (maxwell.py:211-222)."""
+        exact = self.to_padded(mode.evaluate(self.nodes, t))
+        return math.sqrt(max(float(self.mass_norm(u - exact).item()), 0.0))
+
+
+def build_b200_operator(mesh: Mesh, elem: ReferenceElement, material: Material = VACUUM,
+                        connectivity: FaceConnectivity | None = None, *,
+                        dtype: torch.dtype = torch.float32, device=None) -> B200MaxwellOperator:
+    """Drop-in for build_reference_operator (oracle.py:97-141) on one B200."""
+    if connectivity is None:
+        connectivity = build_connectivity(mesh)
+    geometry = compute_geometry(mesh, elem)
+    maps = build_face_maps(mesh, elem, connectivity)
+    op = B200MaxwellOperator(elem, material, geometry_words(geometry), geometry.det_jacobians, maps,
+                             dtype=dtype, device=device)
+    op.mesh = mesh
+    op.connectivity = connectivity
+    op.geometry = geometry
+    return op

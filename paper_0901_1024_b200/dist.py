@@ -1,0 +1,313 @@
+"""Element-partitioned multi-GPU operator: one rank per B200, face-trace halo over NVLink.
+
+The reference is single-process; this module adds the one
+parallel strategy the operator admits: contiguous element
+ranges per rank.  Box meshes are numbered ix-major (reference mesh.py:111-121),
+so a contiguous range of whole x-layers of cells is an x-slab and its only
+neighbours are the two adjacent slabs.
+
+Per rank (``RankDomain``):
+  * owned elements get local ids 0..K_own-1 (global order preserved), ghosts
+    (neighbours owned elsewhere) get K_own.. sorted by global id, i.e. grouped
+    by owning rank;
+  * ``send[peer]``: local ids of owned elements that are ghosts on ``peer``,
+    in the order the peer stores them; ``recv[peer] = (ghost_begin, count)``;
+  * ``interior = (p, q)``: a contiguous owned range none of whose elements
+    reads a ghost -- the stage kernel runs on it while the halo is in flight.
+
+Per LSRK stage (``DistributedMaxwellOperator``): on a communication stream,
+pack the boundary elements of u_in (dgm_halo_pack), exchange with NCCL
+send/recv, unpack into the ghost slots (dgm_halo_unpack); meanwhile the
+compute stream runs the fused stage kernel on the interior range; then the
+boundary ranges.  Only scalar diagnostics use an all-reduce.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .facemaps import FaceMaps, build_face_maps
+from .maxwell import VACUUM, Material
+from .mesh import Mesh, box_slab_mesh, build_connectivity, compute_geometry, map_nodes
+from .refelem import NUM_FACES, ReferenceElement
+
+
+def split_range(n: int, parts: int, index: int) -> tuple[int, int]:
+    """Balanced contiguous split of range(n) into ``parts``; returns part ``index``."""
+    base, extra = divmod(int(n), int(parts))
+    begin = index * base + min(index, extra)
+    return begin, begin + base + (1 if index < extra else 0)
+
+
+@dataclass
+class RankDomain:
+    rank: int
+    world: int
+    elem: ReferenceElement
+    owned: tuple[int, int]          # global element range [g0, g1)
+    ghost_global: np.ndarray        # (G,) global ids of ghosts, sorted
+    maps: FaceMaps                  # neighbors in local ids (owned + ghost range)
+    geo_words: np.ndarray           # (K_own, 26)
+    det_j: np.ndarray               # (K_own,)
+    send: dict = field(default_factory=dict)   # peer -> local owned ids (int32)
+    recv: dict = field(default_factory=dict)   # peer -> (ghost_begin, count)
+    interior: tuple[int, int] = (0, 0)
+    owner_ranges: list = field(default_factory=list)  # per rank global [g0, g1)
+    mesh: Mesh | None = None        # submesh holding owned (+ ghost) elements
+    sub_offset: int = 0             # submesh element j <-> global j + sub_offset
+
+    @property
+    def num_owned(self) -> int:
+        return self.owned[1] - self.owned[0]
+
+    @property
+    def num_ghost(self) -> int:
+        return len(self.ghost_global)
+
+    def owned_nodes(self) -> np.ndarray:
+        """(K_own, Np, 3) physical node coordinates of the owned elements."""
+        lo = self.owned[0] - self.sub_offset
+        sub = Mesh(self.mesh.vertices, self.mesh.elements[lo:lo + self.num_owned])
+        return map_nodes(sub, self.elem)
+
+
+def _localize(rank: int, world: int, owner_ranges, nbr_global: np.ndarray, codes: np.ndarray,
+              owned: tuple[int, int]):
+    """Map owned rows' global neighbor ids to local ids; derive ghosts, recv slices, interior range."""
+    g0, g1 = owned
+    k_own = g1 - g0
+    inner = codes >= 0
+    outside = inner & ((nbr_global < g0) | (nbr_global >= g1))
+    ghost_global = np.unique(nbr_global[outside])
+    local = nbr_global.astype(np.int64) - g0
+    if len(ghost_global):
+        local[outside] = k_own + np.searchsorted(ghost_global, nbr_global[outside])
+    local[~inner] = np.arange(k_own)[:, None].repeat(NUM_FACES, 1)[~inner]
+    recv = {}
+    for peer, (p0, p1) in enumerate(owner_ranges):
+        if peer == rank:
+            continue
+        lo, hi = np.searchsorted(ghost_global, [p0, p1])
+        if hi > lo:
+            recv[peer] = (k_own + int(lo), int(hi - lo))
+    touches = outside.any(axis=1)
+    idx = np.flatnonzero(touches)
+    if len(idx) == 0:
+        interior = (0, k_own)
+    else:
+        # largest gap between boundary elements is the interior range
+        edges = np.concatenate(([-1], idx, [k_own]))
+        gaps = np.diff(edges) - 1
+        j = int(np.argmax(gaps))
+        interior = (int(edges[j] + 1), int(edges[j + 1]))
+    return local.astype(np.int32), ghost_global.astype(np.int64), recv, interior
+
+
+def _send_lists(rank: int, world: int, owned, owner_ranges, ghost_lists_of_peers):
+    """Local ids this rank must send to each peer (peer's ghosts owned here, sorted)."""
+    g0, g1 = owned
+    send = {}
+    for peer, ghosts in ghost_lists_of_peers.items():
+        if peer == rank:
+            continue
+        mine = ghosts[(ghosts >= g0) & (ghosts < g1)]
+        if len(mine):
+            send[peer] = (mine - g0).astype(np.int32)
+    return send
+
+
+def _geometry_rows(mesh: Mesh, rows: slice):
+    from .operator import geometry_words
+
+    sub = Mesh(mesh.vertices, mesh.elements[rows])
+    geo = compute_geometry(sub)
+    return geometry_words(geo), geo.det_jacobians
+
+
+def build_box_domain(extent, cells, elem: ReferenceElement, rank: int, world: int) -> RankDomain:
+    """Rank ``rank`` of an x-slab partition of generate_box_mesh(extent, cells), set up locally.
+
+    Each rank meshes only its slab plus one ghost cell layer on each side
+    (O(K/P) host work), which reproduces the global connectivity exactly for
+    the owned elements (tests/test_dist.py).
+    """
+    nx, ny, nz = (int(c) for c in cells)
+    if world > nx:
+        raise ValueError(f"{world} ranks need at least {world} cell layers in x, got {nx}")
+    per_layer = ny * nz * 6
+    layer_ranges = [split_range(nx, world, r) for r in range(world)]
+    owner_ranges = [(a * per_layer, b * per_layer) for a, b in layer_ranges]
+    ix0, ix1 = layer_ranges[rank]
+    lo, hi = max(ix0 - 1, 0), min(ix1 + 1, nx)
+    sub = box_slab_mesh(extent, cells, lo, hi)
+    off = lo * per_layer
+    conn = build_connectivity(sub)
+    maps_sub = build_face_maps(sub, elem, conn)
+    own = slice((ix0 - lo) * per_layer, (ix1 - lo) * per_layer)
+    owned = owner_ranges[rank]
+    nbr_g = maps_sub.neighbors[own].astype(np.int64) + off
+    codes = maps_sub.codes[own].copy()
+    # faces on the slab mesh's artificial x-walls belong to ghost elements only
+    local, ghosts, recv, interior = _localize(rank, world, owner_ranges, nbr_g, codes, owned)
+    # which of my owned elements are ghosts of my neighbours: the cell layers adjacent to them
+    ghost_lists = {}
+    for peer in (rank - 1, rank + 1):
+        if 0 <= peer < world:
+            p0, p1 = layer_ranges[peer]
+            layer = p1 - 1 if peer < rank else p0  # peer's layer adjacent to me
+            # peer's ghosts: my layer adjacent to the peer
+            mine = ix0 if peer < rank else ix1 - 1
+            ids = np.arange(mine * per_layer, (mine + 1) * per_layer)
+            # only elements that actually share a face with the peer's slab
+            ghost_lists[peer] = ids
+            del layer
+    send = {}
+    for peer, ids in ghost_lists.items():
+        # refine: peer's ghosts are exactly the elements with a face neighbor in the peer's range
+        p0, p1 = owner_ranges[peer]
+        rows = ids - owned[0]
+        touching = ((nbr_g[rows] >= p0) & (nbr_g[rows] < p1) & (codes[rows] >= 0)).any(axis=1)
+        send[peer] = rows[touching].astype(np.int32)
+    geo_words, det = _geometry_rows(sub, own)
+    maps = FaceMaps(num_nodes=elem.num_nodes, face_nodes=maps_sub.face_nodes, neighbors=local, codes=codes,
+                    code_table=maps_sub.code_table)
+    return RankDomain(rank=rank, world=world, elem=elem, owned=owned, ghost_global=ghosts, maps=maps,
+                      geo_words=geo_words, det_j=det, send=send, recv=recv, interior=interior,
+                      owner_ranges=owner_ranges, mesh=sub, sub_offset=off)
+
+
+def build_mesh_domain(mesh: Mesh, elem: ReferenceElement, rank: int, world: int,
+                      global_maps: FaceMaps | None = None) -> RankDomain:
+    """Generic partition: contiguous element ranges of an arbitrary mesh (global setup on every rank)."""
+    k = mesh.num_elements
+    owner_ranges = [split_range(k, world, r) for r in range(world)]
+    maps_g = build_face_maps(mesh, elem) if global_maps is None else global_maps
+    owned = owner_ranges[rank]
+    rows = slice(*owned)
+    nbr_g = maps_g.neighbors[rows].astype(np.int64)
+    codes = maps_g.codes[rows].copy()
+    local, ghosts, recv, interior = _localize(rank, world, owner_ranges, nbr_g, codes, owned)
+    ghost_lists = {}
+    for peer in range(world):
+        if peer == rank:
+            continue
+        p0, p1 = owner_ranges[peer]
+        pn, pc = maps_g.neighbors[p0:p1].astype(np.int64), maps_g.codes[p0:p1]
+        out = (pc >= 0) & ((pn < p0) | (pn >= p1))
+        ghost_lists[peer] = np.unique(pn[out])
+    send = _send_lists(rank, world, owned, owner_ranges, ghost_lists)
+    geo_words, det = _geometry_rows(mesh, rows)
+    maps = FaceMaps(num_nodes=elem.num_nodes, face_nodes=maps_g.face_nodes, neighbors=local, codes=codes,
+                    code_table=maps_g.code_table)
+    return RankDomain(rank=rank, world=world, elem=elem, owned=owned, ghost_global=ghosts, maps=maps,
+                      geo_words=geo_words, det_j=det, send=send, recv=recv, interior=interior,
+                      owner_ranges=owner_ranges, mesh=mesh, sub_offset=0)
+
+
+class DistributedMaxwellOperator:
+    """One rank's share of the operator; halo exchange over torch.distributed (NCCL)."""
+
+    def __init__(self, domain: RankDomain, material: Material = VACUUM, *, dtype=None, device=None):
+        import torch
+
+        from .operator import B200MaxwellOperator
+
+        self.domain = domain
+        self.torch = torch
+        dtype = torch.float32 if dtype is None else dtype
+        self.op = B200MaxwellOperator(domain.elem, material, domain.geo_words, domain.det_j, domain.maps,
+                                      num_ghost=domain.num_ghost, dtype=dtype, device=device)
+        self.device = self.op.device
+        self.comm_stream = torch.cuda.Stream(self.device)
+        rows = 6 * self.op.np_stride
+        self._send = {p: (torch.as_tensor(ids, device=self.device),
+                          torch.empty((len(ids), rows), dtype=dtype, device=self.device))
+                      for p, ids in domain.send.items()}
+        self._recv = {p: torch.empty((cnt, rows), dtype=dtype, device=self.device)
+                      for p, (_, cnt) in domain.recv.items()}
+        self._alt = self.op.empty_state()
+        self._res = self.op.empty_state()
+
+    @property
+    def num_elements(self) -> int:
+        return self.op.num_elements
+
+    def to_padded(self, natural_owned):
+        """Owned natural (6, K_own, Np) -> padded local state (ghost slots zero until exchanged)."""
+        return self.op.to_padded(natural_owned)
+
+    def exchange(self, u) -> None:
+        """Fill u's ghost slots from their owners (blocking on the current stream)."""
+        ev = self._exchange_async(u)
+        self.torch.cuda.current_stream(self.device).wait_event(ev)
+
+    def _exchange_async(self, u):
+        torch = self.torch
+        import torch.distributed as dist
+
+        from . import _capi
+
+        lib, plan = self.op._lib, self.op._plan
+        compute = torch.cuda.current_stream(self.device)
+        self.comm_stream.wait_stream(compute)
+        with torch.cuda.stream(self.comm_stream):
+            s = self.comm_stream.cuda_stream
+            for peer, (ids, buf) in self._send.items():
+                _capi.check(lib.dgm_halo_pack(plan, u.data_ptr(), ids.data_ptr(), len(ids), buf.data_ptr(), s),
+                            "dgm_halo_pack")
+            ops = [dist.P2POp(dist.isend, buf, peer) for peer, (_, buf) in self._send.items()]
+            ops += [dist.P2POp(dist.irecv, buf, peer) for peer, buf in self._recv.items()]
+            if ops:
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+            for peer, buf in self._recv.items():
+                begin, cnt = self.domain.recv[peer]
+                _capi.check(lib.dgm_halo_unpack(plan, buf.data_ptr(), cnt, begin, u.data_ptr(), s),
+                            "dgm_halo_unpack")
+            ev = torch.cuda.Event()
+            ev.record(self.comm_stream)
+        return ev
+
+    def _stage(self, u_in, u_out, a, b, dt) -> None:
+        torch = self.torch
+        p, q = self.domain.interior
+        k = self.op.num_elements
+        ev = self._exchange_async(u_in)
+        if q > p:
+            self.op.lsrk_stage(u_in, u_out, self._res, a, b, dt, p, q)
+        torch.cuda.current_stream(self.device).wait_event(ev)
+        if p > 0:
+            self.op.lsrk_stage(u_in, u_out, self._res, a, b, dt, 0, p)
+        if k > q:
+            self.op.lsrk_stage(u_in, u_out, self._res, a, b, dt, q, k)
+
+    def advance(self, u, dt: float, nsteps: int = 1):
+        """nsteps LSRK4 steps of the owned elements (ghosts refreshed every stage)."""
+        from .stepper import RK_A, RK_B
+
+        if dt <= 0.0:
+            raise ValueError("dt must be positive")
+        cur, nxt = u, self._alt
+        for _ in range(int(nsteps)):
+            for a, b in zip(RK_A, RK_B):
+                self._stage(cur, nxt, a, b, dt)
+                cur, nxt = nxt, cur
+        if cur is not u:
+            u.copy_(cur)
+        return u
+
+    def rhs_padded(self, u, out=None):
+        out = self.op.empty_state() if out is None else out
+        self.exchange(u)
+        return self.op.rhs_padded(u, out)
+
+    def field_energy(self, u) -> float:
+        import torch.distributed as dist
+
+        m = self.op.material
+        t = self.op.mass_norm(u, m.permittivity, m.permeability)
+        if dist.is_initialized() and dist.get_world_size() > 1:
+            dist.all_reduce(t)
+        return 0.5 * float(t.item())

@@ -151,25 +151,16 @@ def build_box_domain(extent, cells, elem: ReferenceElement, rank: int, world: in
     codes = maps_sub.codes[own].copy()
     # faces on the slab mesh's artificial x-walls belong to ghost elements only
     local, ghosts, recv, interior = _localize(rank, world, owner_ranges, nbr_g, codes, owned)
-    # which of my owned elements are ghosts of my neighbours: the cell layers adjacent to them
-    ghost_lists = {}
+    # a peer's ghosts owned here: my elements with a face neighbor in the peer's range
+    # (face adjacency is symmetric), in global order -- the order the peer stores them
+    send = {}
     for peer in (rank - 1, rank + 1):
         if 0 <= peer < world:
-            p0, p1 = layer_ranges[peer]
-            layer = p1 - 1 if peer < rank else p0  # peer's layer adjacent to me
-            # peer's ghosts: my layer adjacent to the peer
-            mine = ix0 if peer < rank else ix1 - 1
-            ids = np.arange(mine * per_layer, (mine + 1) * per_layer)
-            # only elements that actually share a face with the peer's slab
-            ghost_lists[peer] = ids
-            del layer
-    send = {}
-    for peer, ids in ghost_lists.items():
-        # refine: peer's ghosts are exactly the elements with a face neighbor in the peer's range
-        p0, p1 = owner_ranges[peer]
-        rows = ids - owned[0]
-        touching = ((nbr_g[rows] >= p0) & (nbr_g[rows] < p1) & (codes[rows] >= 0)).any(axis=1)
-        send[peer] = rows[touching].astype(np.int32)
+            p0, p1 = owner_ranges[peer]
+            touching = ((nbr_g >= p0) & (nbr_g < p1) & (codes >= 0)).any(axis=1)
+            rows = np.flatnonzero(touching)
+            if len(rows):
+                send[peer] = rows.astype(np.int32)
     geo_words, det = _geometry_rows(sub, own)
     maps = FaceMaps(num_nodes=elem.num_nodes, face_nodes=maps_sub.face_nodes, neighbors=local, codes=codes,
                     code_table=maps_sub.code_table)

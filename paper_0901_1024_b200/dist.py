@@ -234,45 +234,64 @@ class DistributedMaxwellOperator:
         ev = self._exchange_async(u)
         self.torch.cuda.current_stream(self.device).wait_event(ev)
 
+    def pack(self, u, stream=None) -> dict:
+        """dgm_halo_pack every send list of u into its send buffer; returns {peer: buffer}."""
+        from . import _capi
+
+        s = self.torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream.cuda_stream
+        for peer, (ids, buf) in self._send.items():
+            _capi.check(self.op._lib.dgm_halo_pack(self.op._plan, u.data_ptr(), ids.data_ptr(), len(ids),
+                                                   buf.data_ptr(), s), "dgm_halo_pack")
+        return {peer: buf for peer, (_, buf) in self._send.items()}
+
+    def unpack(self, u, stream=None) -> None:
+        """dgm_halo_unpack every receive buffer into u's ghost slots."""
+        from . import _capi
+
+        s = self.torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream.cuda_stream
+        for peer, buf in self._recv.items():
+            begin, cnt = self.domain.recv[peer]
+            _capi.check(self.op._lib.dgm_halo_unpack(self.op._plan, buf.data_ptr(), cnt, begin, u.data_ptr(), s),
+                        "dgm_halo_unpack")
+
+    @property
+    def recv_buffers(self) -> dict:
+        return self._recv
+
     def _exchange_async(self, u):
+        """Pack -> NCCL send/recv -> unpack on the communication stream; returns its completion event."""
         torch = self.torch
         import torch.distributed as dist
 
-        from . import _capi
-
-        lib, plan = self.op._lib, self.op._plan
         compute = torch.cuda.current_stream(self.device)
         self.comm_stream.wait_stream(compute)
         with torch.cuda.stream(self.comm_stream):
-            s = self.comm_stream.cuda_stream
-            for peer, (ids, buf) in self._send.items():
-                _capi.check(lib.dgm_halo_pack(plan, u.data_ptr(), ids.data_ptr(), len(ids), buf.data_ptr(), s),
-                            "dgm_halo_pack")
-            ops = [dist.P2POp(dist.isend, buf, peer) for peer, (_, buf) in self._send.items()]
+            sends = self.pack(u, self.comm_stream)
+            ops = [dist.P2POp(dist.isend, buf, peer) for peer, buf in sends.items()]
             ops += [dist.P2POp(dist.irecv, buf, peer) for peer, buf in self._recv.items()]
             if ops:
                 for req in dist.batch_isend_irecv(ops):
                     req.wait()
-            for peer, buf in self._recv.items():
-                begin, cnt = self.domain.recv[peer]
-                _capi.check(lib.dgm_halo_unpack(plan, buf.data_ptr(), cnt, begin, u.data_ptr(), s),
-                            "dgm_halo_unpack")
+            self.unpack(u, self.comm_stream)
             ev = torch.cuda.Event()
             ev.record(self.comm_stream)
         return ev
 
-    def _stage(self, u_in, u_out, a, b, dt) -> None:
-        torch = self.torch
+    def stage_ranges(self):
+        """(interior range, boundary ranges) of the owned elements."""
         p, q = self.domain.interior
         k = self.op.num_elements
+        bnd = [(a, b) for a, b in ((0, p), (q, k)) if b > a]
+        return (p, q), bnd
+
+    def _stage(self, u_in, u_out, a, b, dt) -> None:
+        (p, q), boundary = self.stage_ranges()
         ev = self._exchange_async(u_in)
-        if q > p:
+        if q > p:  # interior elements read no ghost: overlap with the halo exchange
             self.op.lsrk_stage(u_in, u_out, self._res, a, b, dt, p, q)
-        torch.cuda.current_stream(self.device).wait_event(ev)
-        if p > 0:
-            self.op.lsrk_stage(u_in, u_out, self._res, a, b, dt, 0, p)
-        if k > q:
-            self.op.lsrk_stage(u_in, u_out, self._res, a, b, dt, q, k)
+        self.torch.cuda.current_stream(self.device).wait_event(ev)
+        for lo, hi in boundary:
+            self.op.lsrk_stage(u_in, u_out, self._res, a, b, dt, lo, hi)
 
     def advance(self, u, dt: float, nsteps: int = 1):
         """nsteps LSRK4 steps of the owned elements (ghosts refreshed every stage)."""

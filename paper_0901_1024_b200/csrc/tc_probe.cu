@@ -1,0 +1,94 @@
+// tc_probe.cu -- test-only probe of the tcgen05 kind::tf32 path (libdgm_probe.so).
+//
+// C[128 x N] = A[128 x K] * B[N x K]^T with 1 (plain TF32) or 3 (3xTF32:
+// hi*hi + lo*hi + hi*lo) MMA passes, operands staged in the K-major
+// SWIZZLE_NONE layout of tc05.cuh, accumulator in TMEM, read back with
+// tcgen05.ld.  tests/test_gpu_tc05.py compares it with an fp64 product.
+#include <cuda_runtime.h>
+
+#include "tc05.cuh"
+
+namespace {
+
+__global__ void __launch_bounds__(128) probe_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                    float* __restrict__ c, int n, int k, int passes) {
+  using namespace dgm::tc;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int m = 128;
+  float* a_hi = reinterpret_cast<float*>(smem);
+  float* a_lo = a_hi + m * k;
+  float* b_hi = a_lo + m * k;
+  float* b_lo = b_hi + n * k;
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  for (int i = tid; i < m * k; i += blockDim.x) {
+    const int r = i / k, q = i - r * k;
+    const int off = ((q >> 2) * m + r) * 4 + (q & 3);
+    float hi, lo;
+    split_tf32(a[i], hi, lo);
+    a_hi[off] = hi;
+    a_lo[off] = lo;
+  }
+  for (int i = tid; i < n * k; i += blockDim.x) {
+    const int r = i / k, q = i - r * k;
+    const int off = ((q >> 2) * n + r) * 4 + (q & 3);
+    float hi, lo;
+    split_tf32(b[i], hi, lo);
+    b_hi[off] = hi;
+    b_lo[off] = lo;
+  }
+  if (warp == 0) tmem_alloc(&tmem_base, 256);
+  if (tid == 32) {
+    mbar_init(&mbar, 1);
+    mbar_init_fence();
+  }
+  fence_async_smem();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+
+  if (tid == 0) {
+    const uint32_t idesc = idesc_tf32(m, n);
+    for (int s = 0; s < k / 8; ++s) {
+      const uint32_t ao = s * 2 * m * 16, bo = s * 2 * n * 16;
+      const uint64_t ah = desc_kmajor(smem_u32(a_hi) + ao, m * 16, 128);
+      const uint64_t al = desc_kmajor(smem_u32(a_lo) + ao, m * 16, 128);
+      const uint64_t bh = desc_kmajor(smem_u32(b_hi) + bo, n * 16, 128);
+      const uint64_t bl = desc_kmajor(smem_u32(b_lo) + bo, n * 16, 128);
+      mma_tf32(tmem, ah, bh, idesc, s > 0);
+      if (passes == 3) {
+        mma_tf32(tmem, al, bh, idesc, 1);
+        mma_tf32(tmem, ah, bl, idesc, 1);
+      }
+    }
+    mma_commit(&mbar);
+  }
+  mbar_wait(&mbar, 0);
+  fence_after_sync();
+  const int row = warp * 32 + (tid & 31);
+  for (int col = 0; col < n; col += 8) {
+    float v[8];
+    tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + col, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[row * n + col + j] = v[j];
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
+}  // namespace
+
+extern "C" int dgm_probe_tf32_gemm(const float* a, const float* b, float* c, int n, int k, int passes,
+                                   void* stream) {
+  if (n < 8 || n > 256 || n % 8 || k < 8 || k > 64 || k % 8 || (passes != 1 && passes != 3)) return -1;
+  const size_t smem = (size_t)2 * (128 + n) * k * sizeof(float);
+  if (cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return -2;
+  probe_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(a, b, c, n, k, passes);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}

@@ -62,7 +62,15 @@ typedef struct {
   int32_t tile_elements;    /* elements per CTA tile of the stage kernel    */
   int32_t threads;          /* threads per CTA of the stage kernel          */
   int64_t smem_bytes_fixed; /* dynamic smem per CTA excluding code table    */
+  /* tensor-core (tcgen05, 3xTF32) stage path, f32 and N <= 4 only */
+  int32_t tc_supported;     /* 1 if this order/dtype has the tensor-core path */
+  int32_t tc_nb;            /* MMA N: Np rounded up to 16                     */
+  int32_t tc_steps;         /* K steps of 8 (K = 3*tc_npk + 4*Nfp, padded)     */
+  int32_t tc_npk;           /* K extent of one derivative block (Np up to 4)  */
+  int64_t tc_operand_floats;/* size of dgm_desc.tc_operand in floats          */
 } dgm_layout_info;
+
+enum { DGM_PATH_AUTO = 0, DGM_PATH_SIMT = 1, DGM_PATH_TENSOR = 2 };
 
 /*
  * Operator description (replaces build_reference_operator, oracle.py:97-141).
@@ -84,6 +92,12 @@ typedef struct {
  *  face_nodes  : uint8[4][Nfp]            elem.face_nodes (refelem.py:387-394)
  *  code_table  : uint8[num_codes][Nfp]    vmap_plus rows minus neighbor*Np
  *                (oracle.py:116-123)
+ *  tc_operand  : float[tc_steps][2][2][tc_nb][4], the constant GEMM operand
+ *                B[n][k] = [D_r | D_s | D_t | LIFT][n][k] (derivative blocks
+ *                tc_npk wide, zero padded) split into tf32 hi / exact lo parts:
+ *                tc_operand[s][h][c][n][q] = part_h(B[n][8s + 4c + q]).
+ *                NULL disables the tensor-core path.
+ *  path        : DGM_PATH_AUTO (tensor cores when available), _SIMT or _TENSOR.
  */
 typedef struct {
   int32_t order;
@@ -100,6 +114,8 @@ typedef struct {
   int32_t num_codes;
   double permittivity;    /* Material.permittivity (maxwell.py:23-47) */
   double permeability;
+  const void* tc_operand;
+  int32_t path;
 } dgm_desc;
 
 typedef struct dgm_plan dgm_plan;
@@ -116,6 +132,9 @@ int dgm_layout(int32_t order, int32_t dtype, dgm_layout_info* out);
 /* Validates the description, stores it, and configures kernel attributes. */
 int dgm_plan_create(const dgm_desc* desc, dgm_plan** out);
 int dgm_plan_destroy(dgm_plan* plan);
+
+/* Path the stage kernels of a plan run on: DGM_PATH_SIMT or DGM_PATH_TENSOR. */
+int dgm_plan_path(const dgm_plan* plan);
 
 /*
  * Full semidiscrete RHS on elements [e_begin, e_end) of the padded state u

@@ -13,10 +13,12 @@ from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdgm.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 GEO_WORDS = 26
 
 DGM_F32, DGM_F64 = 0, 1
+PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2
+PATHS = {"auto": PATH_AUTO, "simt": PATH_SIMT, "tensor": PATH_TENSOR}
 _ERR_NAMES = {-1: "invalid argument", -2: "CUDA error", -3: "unsupported"}
 
 
@@ -30,7 +32,9 @@ class LayoutInfo(ctypes.Structure):
                 ("np_stride", ctypes.c_int32), ("diff_chunks", ctypes.c_int32),
                 ("lift_chunks", ctypes.c_int32), ("vec", ctypes.c_int32),
                 ("tile_elements", ctypes.c_int32), ("threads", ctypes.c_int32),
-                ("smem_bytes_fixed", ctypes.c_int64)]
+                ("smem_bytes_fixed", ctypes.c_int64), ("tc_supported", ctypes.c_int32),
+                ("tc_nb", ctypes.c_int32), ("tc_steps", ctypes.c_int32), ("tc_npk", ctypes.c_int32),
+                ("tc_operand_floats", ctypes.c_int64)]
 
 
 class Desc(ctypes.Structure):
@@ -40,7 +44,8 @@ class Desc(ctypes.Structure):
                 ("geometry", ctypes.c_void_p), ("neighbors", ctypes.c_void_p),
                 ("codes", ctypes.c_void_p), ("face_nodes", ctypes.c_void_p),
                 ("code_table", ctypes.c_void_p), ("num_codes", ctypes.c_int32),
-                ("permittivity", ctypes.c_double), ("permeability", ctypes.c_double)]
+                ("permittivity", ctypes.c_double), ("permeability", ctypes.c_double),
+                ("tc_operand", ctypes.c_void_p), ("path", ctypes.c_int32)]
 
 
 _I64, _VP, _D = ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
@@ -50,6 +55,7 @@ _SIGNATURES = {
     "dgm_layout": ([ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(LayoutInfo)], ctypes.c_int),
     "dgm_plan_create": ([ctypes.POINTER(Desc), ctypes.POINTER(_VP)], ctypes.c_int),
     "dgm_plan_destroy": ([_VP], ctypes.c_int),
+    "dgm_plan_path": ([_VP], ctypes.c_int),
     "dgm_rhs": ([_VP, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
     "dgm_lsrk_stage": ([_VP, _VP, _VP, _VP, _D, _D, _D, _I64, _I64, _VP], ctypes.c_int),
     "dgm_volume": ([_VP, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
@@ -104,6 +110,11 @@ class Layout:
     tile_elements: int
     threads: int
     smem_bytes_fixed: int
+    tc_supported: int
+    tc_nb: int
+    tc_steps: int
+    tc_npk: int
+    tc_operand_floats: int
 
 
 def layout(order: int, dtype: int) -> Layout:

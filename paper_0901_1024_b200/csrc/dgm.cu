@@ -12,8 +12,9 @@
 #include "../../include/dgm.h"
 #include "dgm_aux.cuh"
 #include "dgm_stage.cuh"
+#include "dgm_tc.cuh"
 
-#define DGM_ABI_VERSION 1
+#define DGM_ABI_VERSION 2
 
 namespace {
 
@@ -64,8 +65,33 @@ int grid_for(int64_t work, int threads) {
 
 struct dgm_plan {
   dgm_desc d;
-  size_t stage_smem;  // dynamic smem of the stage kernels
+  size_t stage_smem;  // dynamic smem of the SIMT stage kernels
+  int path;           // DGM_PATH_SIMT or DGM_PATH_TENSOR
+  size_t tc_smem;     // dynamic smem of the tensor-core stage kernels
+  int num_sms;
 };
+
+namespace {
+template <int N, typename T>
+struct TcInfo {
+  static constexpr bool supported = false;
+  static constexpr int nb = 0, steps = 0, npk = 0;
+  static constexpr int64_t floats = 0;
+};
+#define DGM_TC_INFO(n)                                                   \
+  template <>                                                            \
+  struct TcInfo<n, float> {                                              \
+    static constexpr bool supported = true;                              \
+    static constexpr int nb = dgm::TcCfg<n>::NB, steps = dgm::TcCfg<n>::KS; \
+    static constexpr int npk = dgm::TcCfg<n>::NPK;                       \
+    static constexpr int64_t floats = (int64_t)dgm::TcCfg<n>::B_FLOATS;  \
+  };
+DGM_TC_INFO(1)
+DGM_TC_INFO(2)
+DGM_TC_INFO(3)
+DGM_TC_INFO(4)
+#undef DGM_TC_INFO
+}  // namespace
 
 extern "C" {
 
@@ -88,6 +114,12 @@ int dgm_layout(int32_t order, int32_t dtype, dgm_layout_info* out) {
     out->tile_elements = C::TE;
     out->threads = C::THREADS;
     out->smem_bytes_fixed = (int64_t)C::SMEM_FIXED;
+    using TI = TcInfo<decltype(n)::value, decltype(t)>;
+    out->tc_supported = TI::supported ? 1 : 0;
+    out->tc_nb = TI::nb;
+    out->tc_steps = TI::steps;
+    out->tc_npk = TI::npk;
+    out->tc_operand_floats = TI::floats;
     return DGM_OK;
   });
 }
@@ -144,10 +176,52 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
     return DGM_OK;
   });
   if (rc) return rc;
+  if (d.path < DGM_PATH_AUTO || d.path > DGM_PATH_TENSOR) return fail(DGM_ERR_INVALID, "bad path %d", d.path);
+  int path = DGM_PATH_SIMT;
+  size_t tc_smem = 0;
+  rc = dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    if constexpr (TcInfo<N, T>::supported) {
+      if (d.path == DGM_PATH_SIMT) return DGM_OK;
+      if (!d.tc_operand || !aligned16(d.tc_operand)) {
+        if (d.path == DGM_PATH_TENSOR)
+          return fail(DGM_ERR_INVALID, "tensor path requested without a 16-byte aligned tc_operand");
+        return DGM_OK;
+      }
+      using TC = dgm::TcCfg<N>;
+      tc_smem = (TC::SMEM_FIXED + (size_t)d.num_codes * TC::NFP + 127) & ~size_t(127);
+      if (tc_smem > 227 * 1024) {
+        if (d.path == DGM_PATH_TENSOR) return fail(DGM_ERR_UNSUPPORTED, "tensor path smem %zu too large", tc_smem);
+        return DGM_OK;
+      }
+      int r;
+      if ((r = cuda_check(cudaFuncSetAttribute(dgm::tc_stage_kernel<N, dgm::MODE_RHS>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem),
+                          "cudaFuncSetAttribute(tc)")))
+        return r;
+      if ((r = cuda_check(cudaFuncSetAttribute(dgm::tc_stage_kernel<N, dgm::MODE_LSRK>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem),
+                          "cudaFuncSetAttribute(tc)")))
+        return r;
+      path = DGM_PATH_TENSOR;
+      return DGM_OK;
+    } else {
+      if (d.path == DGM_PATH_TENSOR)
+        return fail(DGM_ERR_UNSUPPORTED, "no tensor-core path for order %d dtype %d", d.order, d.dtype);
+      return DGM_OK;
+    }
+  });
+  if (rc) return rc;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   dgm_plan* p = new (std::nothrow) dgm_plan;
   if (!p) return fail(DGM_ERR_INVALID, "out of host memory");
   p->d = d;
   p->stage_smem = smem;
+  p->path = path;
+  p->tc_smem = tc_smem;
+  p->num_sms = sms > 0 ? sms : 148;
   *out = p;
   return DGM_OK;
 }
@@ -155,6 +229,11 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
 int dgm_plan_destroy(dgm_plan* plan) {
   delete plan;
   return DGM_OK;
+}
+
+int dgm_plan_path(const dgm_plan* plan) {
+  if (!plan) return fail(DGM_ERR_INVALID, "null plan");
+  return plan->path;
 }
 
 }  // extern "C"
@@ -209,6 +288,19 @@ int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, vo
     args.yp = (T)(1.0 / z);
     args.inv_2z = (T)(1.0 / (2.0 * z));
     args.inv_2y = (T)(1.0 / (2.0 * (1.0 / z)));
+    if constexpr (TcInfo<N, T>::supported && (MODE == dgm::MODE_RHS || MODE == dgm::MODE_LSRK)) {
+      if (plan->path == DGM_PATH_TENSOR) {
+        using TC = dgm::TcCfg<N>;
+        dgm::TcArgs targs;
+        targs.s = args;
+        targs.bpack = static_cast<const float*>(d.tc_operand);
+        const int64_t tt = (e_end - e_begin + TC::TE - 1) / TC::TE;
+        targs.num_tiles = (int)tt;
+        const int grid = (int)(tt < plan->num_sms ? tt : plan->num_sms);
+        dgm::tc_stage_kernel<N, MODE><<<grid, TC::THREADS, plan->tc_smem, static_cast<cudaStream_t>(stream)>>>(targs);
+        return cuda_check(cudaGetLastError(), "tc_stage_kernel launch");
+      }
+    }
     const int64_t tiles = (e_end - e_begin + C::TE - 1) / C::TE;
     dgm::stage_kernel<N, T, MODE><<<(unsigned)tiles, C::THREADS, plan->stage_smem,
                                     static_cast<cudaStream_t>(stream)>>>(args);

@@ -1,0 +1,378 @@
+// dgm_tc.cuh -- fused Maxwell stage kernel on the 5th-gen tensor cores (fp32 via 3xTF32).
+//
+// The whole semidiscrete RHS of one component c is a single GEMM row per
+// element (oracle.py:67-93 regrouped):
+//
+//   rhs_c = sum_mu D_mu w_mu^(c) + LIFT f^(c)
+//   w_mu^(c) = (sum over the curl's two terms of +-rx[mu][nu] u_g) / (eps|mu)
+//   f^(c)    = upwind_bracket_c * face_jacobian / det_J / (eps|mu)
+//
+// because d/dx_nu u = sum_mu rx[mu][nu] D_mu u and rx is constant per element.
+// So with A[e][k] = [w_0 | w_1 | w_2 | f] (K = 3*NPK + 4*Nfp) and the constant
+// B[n][k] = [D_0 | D_1 | D_2 | LIFT] (rows n = output node), one tcgen05.mma
+// chain per component computes the full RHS of 128 elements (M = 128 lanes
+// of TMEM, one element per lane).  fp32 accuracy comes from 3xTF32
+// (A_hi B_hi + A_lo B_hi + A_hi B_lo) with exact hi/lo splits.
+//
+// Roles (288 threads, one CTA per SM, persistent over 128-element tiles):
+//   warps 0-7 producers: build A K-steps in registers and tcgen05.st them to
+//     TMEM (warps 0-3: E components from H fields, warps 4-7: H components from
+//     E fields; thread = element row = TMEM lane), copy the B K-step into smem;
+//     the surface flux of a K-step is first computed with a face-node-major
+//     mapping (coalesced neighbor gathers) into smem and transposed;
+//     then the epilogue: TMEM accumulators -> smem -> coalesced LSRK update.
+//   warp 8 lane 0: bulk-copies the u tile (cp.async.bulk, mbarrier tx) and
+//     issues the 18 MMAs of every K-step (A from TMEM, B from smem).
+// TMEM: [0, 6*NB) accumulators; two A stages of 6 x (8 hi + 8 lo) columns.
+#pragma once
+
+#include "dgm_stage.cuh"
+#include "tc05.cuh"
+
+namespace dgm {
+
+template <int N>
+struct TcCfg {
+  using C = Cfg<N, float>;
+  static constexpr int NP = C::NP, NFP = C::NFP, NF4 = C::NF4, NPG = C::NPG;
+  static constexpr int NPK = (NP + 3) / 4 * 4;     // K extent of one volume block
+  static constexpr int NB = (NP + 15) / 16 * 16;   // MMA N (M=128, A in TMEM: N % 16 == 0)
+  static constexpr int KV = 3 * NPK;               // volume part of K
+  static constexpr int KT = KV + NF4;
+  static constexpr int KS = (KT + 7) / 8;          // K steps (one kind::tf32 MMA each)
+  static constexpr int TE = 128;
+  static constexpr int PROD = 256;                 // producer threads (8 warps)
+  static constexpr int THREADS = PROD + 32;
+  static constexpr int ACC_COLS = 6 * NB;
+  static constexpr int A_COL0 = (ACC_COLS + 31) / 32 * 32;
+  static constexpr int A_STAGE_COLS = 6 * 16;      // 6 components x (8 hi + 8 lo)
+  static constexpr int TMEM_COLS = 512;
+  static_assert(A_COL0 + 2 * A_STAGE_COLS <= TMEM_COLS, "TMEM budget");
+  static constexpr int SROW = TE + 4;              // flux staging row stride (conflict-free both ways)
+  static constexpr int B_STAGE_BYTES = 2 * 2 * NB * 16;  // hi/lo x 2 chunks x NB rows x 16 B
+  // shared-memory carve-up (bytes)
+  static constexpr size_t OFF_U = 0;
+  static constexpr size_t OFF_GEO = OFF_U + (size_t)6 * TE * NPG * 4;
+  static constexpr size_t OFF_NBR = OFF_GEO + (size_t)TE * GEO_WORDS * 4;
+  static constexpr size_t OFF_CODE = OFF_NBR + (size_t)TE * 4 * 4;
+  static constexpr size_t STAGE_BYTES = (size_t)2 * 6 * 8 * SROW * 4 > (size_t)2 * TE * NPG * 4
+                                            ? (size_t)2 * 6 * 8 * SROW * 4
+                                            : (size_t)2 * TE * NPG * 4;
+  static constexpr size_t OFF_STAGE = OFF_CODE + (size_t)TE * 4 * 4;
+  static constexpr size_t OFF_B = OFF_STAGE + STAGE_BYTES;
+  static constexpr size_t OFF_BAR = OFF_B + (size_t)2 * B_STAGE_BYTES;
+  static constexpr size_t OFF_FMASK = OFF_BAR + 64;
+  static constexpr size_t OFF_PTAB = OFF_FMASK + (4 * NFP + 15) / 16 * 16;
+  static constexpr size_t SMEM_FIXED = OFF_PTAB;   // + ncodes * NFP
+  static constexpr size_t B_FLOATS = (size_t)KS * 2 * 2 * NB * 4;  // packed operand in global
+};
+
+struct TcArgs {
+  StageArgs<float> s;
+  const float* bpack;  // [KS][hi,lo][2 chunks][NB][4]
+  int num_tiles;
+};
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const TcArgs args) {
+  using T = TcCfg<N>;
+  using namespace tc;
+  constexpr int TE = T::TE, NPG = T::NPG, NP = T::NP, NFP = T::NFP, NB = T::NB;
+  constexpr int KS = T::KS, KV = T::KV, KT = T::KT, NPK = T::NPK, SROW = T::SROW;
+  const StageArgs<float>& a = args.s;
+
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* s_u = reinterpret_cast<float*>(smem + T::OFF_U);
+  float* s_geo = reinterpret_cast<float*>(smem + T::OFF_GEO);
+  int* s_nbr = reinterpret_cast<int*>(smem + T::OFF_NBR);
+  int* s_code = reinterpret_cast<int*>(smem + T::OFF_CODE);
+  float* s_stage = reinterpret_cast<float*>(smem + T::OFF_STAGE);
+  unsigned char* s_b = smem + T::OFF_B;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
+  uint64_t* full = bar + 0;      // [2] producers -> MMA
+  uint64_t* empty = bar + 2;     // [2] MMA commit -> producers
+  uint64_t* load_full = bar + 4; // u tile landed
+  uint64_t* acc_full = bar + 5;  // accumulators final
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 6);
+  uint8_t* s_fmask = smem + T::OFF_FMASK;
+  uint8_t* s_ptab = smem + T::OFF_PTAB;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t fstride = a.kf * NPG;
+
+  if (warp == 0) tmem_alloc(s_tmem, T::TMEM_COLS);
+  if (tid == T::PROD) {
+    mbar_init(&full[0], 8);
+    mbar_init(&full[1], 8);
+    mbar_init(&empty[0], 1);
+    mbar_init(&empty[1], 1);
+    mbar_init(load_full, 1);
+    mbar_init(acc_full, 1);
+    mbar_init_fence();
+  }
+  for (int c = tid; c < 4 * NFP; c += blockDim.x) s_fmask[c] = a.fmask[c];
+  for (int c = tid; c < a.ncodes * NFP; c += blockDim.x) s_ptab[c] = a.ptab[c];
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = *s_tmem;
+
+  // per-thread role constants
+  const int quad = warp & 3;           // TMEM lane quadrant
+  const int grp = (warp >> 2) & 1;     // 0: E components (from H fields), 1: H components (from E fields)
+  const int row = quad * 32 + lane;    // element row owned in thread-per-row phases
+  const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
+  const float inv_m = grp == 0 ? a.inv_eps : a.inv_mu;
+  const uint32_t idesc = idesc_tf32(128, NB);
+
+  uint32_t pstep = 0;  // producer K-step counter (all tiles)
+  uint32_t mstep = 0;  // MMA K-step counter
+  int it = 0;
+  for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+    const int64_t e0 = a.e_begin + (int64_t)tile * TE;
+    const int nv = (int)min((int64_t)TE, a.e_end - e0);
+    __syncthreads();  // previous tile's epilogue is done with s_u / s_stage
+
+    if (warp == 8) {
+      if (lane == 0) {
+        const uint32_t rowbytes = (uint32_t)nv * NPG * 4;
+        mbar_expect_tx(load_full, 6 * rowbytes);
+        for (int f = 0; f < 6; ++f)
+          bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowbytes, load_full);
+        const int nt = tile + gridDim.x;  // warm L2 with the next tile of this CTA
+        if (nt < args.num_tiles) {
+          const int64_t n0 = a.e_begin + (int64_t)nt * TE;
+          const uint32_t nb = (uint32_t)min((int64_t)TE, a.e_end - n0) * NPG * 4;
+          for (int f = 0; f < 6; ++f) prefetch_l2(a.u + (int64_t)f * fstride + n0 * NPG, nb);
+        }
+        // ---------------- MMA issuer ----------------
+        for (int s = 0; s < KS; ++s, ++mstep) {
+          const int slot = mstep & 1;
+          mbar_wait(&full[slot], (mstep >> 1) & 1);
+          fence_after_sync();
+          const uint32_t bh = smem_u32(s_b + slot * T::B_STAGE_BYTES);
+          const uint64_t dbh = desc_kmajor(bh, NB * 16, 128);
+          const uint64_t dbl = desc_kmajor(bh + 2 * NB * 16, NB * 16, 128);
+#pragma unroll
+          for (int c = 0; c < 6; ++c) {
+            const uint32_t acc = tmem + c * NB;
+            const uint32_t ah = tmem + T::A_COL0 + slot * T::A_STAGE_COLS + c * 16;
+            mma_tf32_ts(acc, ah, dbh, idesc, s > 0 ? 1u : 0u);
+            mma_tf32_ts(acc, ah + 8, dbh, idesc, 1u);
+            mma_tf32_ts(acc, ah, dbl, idesc, 1u);
+          }
+          mma_commit(&empty[slot]);
+        }
+        mma_commit(acc_full);
+      }
+      __syncwarp();
+      continue;
+    }
+
+    // ================= producers (warps 0-7) =================
+    // per-tile small data: geometry rows, neighbor ids, codes
+    for (int c = tid; c < TE * GEO_WORDS; c += T::PROD)
+      s_geo[c] = (c < nv * GEO_WORDS) ? a.geo[e0 * GEO_WORDS + c] : 0.0f;
+    for (int c = tid; c < TE * 4; c += T::PROD) {
+      const bool ok = c < nv * 4;
+      s_nbr[c] = ok ? a.nbr[e0 * 4 + c] : 0;
+      s_code[c] = ok ? a.code[e0 * 4 + c] : -1;
+    }
+    mbar_wait(load_full, it & 1);
+    named_sync(1, T::PROD);
+
+    // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu
+    float prx[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) prx[q] = s_geo[row * GEO_WORDS + q] * inv_m;
+    const bool row_ok = row < nv;
+
+    for (int s = 0; s < KS; ++s, ++pstep) {
+      const int slot = pstep & 1;
+      float* stg = s_stage + (s & 1) * (6 * 8 * SROW);
+      const int k0 = s * 8;
+      // ---- surface flux of this step's face nodes, face-node-major mapping ----
+      if (k0 + 8 > KV && k0 < KT) {
+#pragma unroll 1
+        for (int item = tid; item < TE * 8; item += T::PROD) {
+          const int r = item >> 3, qq = item & 7;
+          const int q = k0 + qq - KV;
+          if (q < 0 || q >= T::NF4) continue;
+          float out[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (r < nv) {
+            const int face = q / NFP, node = q - face * NFP;
+            const int im = s_fmask[face * NFP + node];
+            float um[6], up[6];
+#pragma unroll
+            for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + r) * NPG + im];
+            const float* gk = s_geo + r * GEO_WORDS;
+            const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
+            const int code = s_code[r * 4 + face];
+            if (code < 0) {
+              const float nde = nx * um[0] + ny * um[1] + nz * um[2];
+              const float ndh = nx * um[3] + ny * um[4] + nz * um[5];
+              up[0] = -um[0] + 2.f * nde * nx;
+              up[1] = -um[1] + 2.f * nde * ny;
+              up[2] = -um[2] + 2.f * nde * nz;
+              up[3] = um[3] - 2.f * ndh * nx;
+              up[4] = um[4] - 2.f * ndh * ny;
+              up[5] = um[5] - 2.f * ndh * nz;
+            } else {
+              const int nb = s_nbr[r * 4 + face];
+              const int jn = s_ptab[code * NFP + node];
+              const int64_t loc = (int64_t)nb - e0;
+              if (loc >= 0 && loc < nv) {
+#pragma unroll
+                for (int f = 0; f < 6; ++f) up[f] = s_u[(f * TE + (int)loc) * NPG + jn];
+              } else {
+                const float* p = a.u + (int64_t)nb * NPG + jn;
+#pragma unroll
+                for (int f = 0; f < 6; ++f) up[f] = __ldg(p + f * fstride);
+              }
+            }
+            upwind(um, up, nx, ny, nz, a, out);
+            const float sc = gk[22 + face] * gk[9];
+#pragma unroll
+            for (int f = 0; f < 3; ++f) out[f] *= sc * a.inv_eps;
+#pragma unroll
+            for (int f = 3; f < 6; ++f) out[f] *= sc * a.inv_mu;
+          }
+#pragma unroll
+          for (int c = 0; c < 6; ++c) stg[(c * 8 + qq) * SROW + r] = out[c];
+        }
+        named_sync(1, T::PROD);
+      }
+
+      // ---- B K-step into smem and A K-step into TMEM (thread-per-row) ----
+      mbar_wait(&empty[slot], ((pstep >> 1) & 1) ^ 1);
+      fence_after_sync();
+      {
+        constexpr int BV = T::B_STAGE_BYTES / 16;
+        if (tid < BV) {
+          const float4* src = reinterpret_cast<const float4*>(args.bpack) + (size_t)s * BV + tid;
+          reinterpret_cast<float4*>(s_b + slot * T::B_STAGE_BYTES)[tid] = __ldg(src);
+          fence_async_smem();
+        }
+      }
+      float v[3][8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = k0 + 4 * h;
+        if (k < KV) {
+          const int mu = k / NPK, j0 = k - mu * NPK;
+          const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
+          const int fb = grp == 0 ? 3 : 0;  // E comps read H fields and vice versa
+          float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + 0) * TE + row) * NPG + j0);
+          float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + 1) * TE + row) * NPG + j0);
+          float4 z = *reinterpret_cast<const float4*>(s_u + ((fb + 2) * TE + row) * NPG + j0);
+          const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w}, zs[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (grp == 0) {  // (curl H)_x,y,z
+              v[0][4 * h + q] = p1 * zs[q] - p2 * ys[q];
+              v[1][4 * h + q] = p2 * xs[q] - p0 * zs[q];
+              v[2][4 * h + q] = p0 * ys[q] - p1 * xs[q];
+            } else {         // -(curl E)_x,y,z
+              v[0][4 * h + q] = p2 * ys[q] - p1 * zs[q];
+              v[1][4 * h + q] = p0 * zs[q] - p2 * xs[q];
+              v[2][4 * h + q] = p1 * xs[q] - p0 * ys[q];
+            }
+          }
+        } else if (k < KT) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[c][4 * h + q] = stg[((3 * grp + c) * 8 + 4 * h + q) * SROW + row];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[c][4 * h + q] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float hi[8], lo[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float x = row_ok ? v[c][q] : 0.f;
+          split_tf32(x, hi[q], lo[q]);
+        }
+        const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + (3 * grp + c) * 16;
+        tmem_st8(tmem + lane_addr + col, hi);
+        tmem_st8(tmem + lane_addr + col + 8, lo);
+      }
+      tmem_st_wait();
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[slot]);
+    }
+
+    // ================= epilogue: accumulators -> LSRK update =================
+    mbar_wait(acc_full, it & 1);
+    fence_after_sync();
+    float* es = s_stage;  // [2][TE][NPG]
+#pragma unroll 1
+    for (int round = 0; round < 3; ++round) {
+      const int comp = 2 * round + grp;
+      {
+        float* dst = es + (grp * TE + row) * NPG;
+#pragma unroll
+        for (int c0 = 0; c0 < NB; c0 += 8) {
+          float r8[8];
+          tmem_ld8(tmem + lane_addr + comp * NB + c0, r8);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 8; q += 4) {
+            const int i = c0 + q;
+            if (i < NPG) {
+              float4 o;
+              o.x = (i + 0 < NP) ? r8[q + 0] : 0.f;
+              o.y = (i + 1 < NP) ? r8[q + 1] : 0.f;
+              o.z = (i + 2 < NP) ? r8[q + 2] : 0.f;
+              o.w = (i + 3 < NP) ? r8[q + 3] : 0.f;
+              *reinterpret_cast<float4*>(dst + i) = o;
+            }
+          }
+        }
+      }
+      named_sync(1, T::PROD);
+      constexpr int RV = NPG / 4;
+      const int nvec = nv * RV;
+#pragma unroll 1
+      for (int g2 = 0; g2 < 2; ++g2) {
+        const int f = 2 * round + g2;
+        const int64_t gbase = ((int64_t)f * a.kf + e0) * NPG;
+        const float4* rs = reinterpret_cast<const float4*>(es + g2 * TE * NPG);
+        const float4* us = reinterpret_cast<const float4*>(s_u + f * TE * NPG);
+        for (int c = tid; c < nvec; c += T::PROD) {
+          const float4 rh = rs[c];
+          const int64_t go = gbase + (int64_t)c * 4;
+          if (MODE == MODE_RHS) {
+            *reinterpret_cast<float4*>(a.out + go) = rh;
+          } else {
+            float4 r;
+            if (a.a_zero) {
+              r = make_float4(a.dt * rh.x, a.dt * rh.y, a.dt * rh.z, a.dt * rh.w);
+            } else {
+              const float4 ro = *reinterpret_cast<const float4*>(a.res + go);
+              r = make_float4(a.a * ro.x + a.dt * rh.x, a.a * ro.y + a.dt * rh.y, a.a * ro.z + a.dt * rh.z,
+                              a.a * ro.w + a.dt * rh.w);
+            }
+            *reinterpret_cast<float4*>(a.res + go) = r;
+            const float4 uo = us[c];
+            *reinterpret_cast<float4*>(a.u_out + go) =
+                make_float4(uo.x + a.b * r.x, uo.y + a.b * r.y, uo.z + a.b * r.z, uo.w + a.b * r.w);
+          }
+        }
+      }
+      named_sync(1, T::PROD);
+    }
+    fence_before_sync();
+  }
+  __syncthreads();
+  fence_after_sync();
+  if (warp == 0) tmem_dealloc(tmem, T::TMEM_COLS);
+}
+
+}  // namespace dgm

@@ -81,7 +81,85 @@ __global__ void __launch_bounds__(128) probe_kernel(const float* __restrict__ a,
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
+// Same product with A written to TMEM by tcgen05.st (row r = lane r) and the TS-form MMA.
+__global__ void __launch_bounds__(128) probe_ts_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                       float* __restrict__ c, int n, int k, int passes) {
+  using namespace dgm::tc;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  float* b_hi = reinterpret_cast<float*>(smem);
+  float* b_lo = b_hi + n * k;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < n * k; i += blockDim.x) {
+    const int r = i / k, q = i - r * k;
+    const int off = ((q >> 2) * n + r) * 4 + (q & 3);
+    float hi, lo;
+    split_tf32(b[i], hi, lo);
+    b_hi[off] = hi;
+    b_lo[off] = lo;
+  }
+  if (warp == 0) tmem_alloc(&tmem_base, 512);
+  if (tid == 32) {
+    mbar_init(&mbar, 1);
+    mbar_init_fence();
+  }
+  fence_async_smem();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  const uint32_t a_hi_col = 256, a_lo_col = 256 + 64;
+  const int row = tid;  // warp w covers lanes 32w..32w+31
+  const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+  for (int k0 = 0; k0 < k; k0 += 8) {
+    float hi[8], lo[8];
+    for (int q = 0; q < 8; ++q) split_tf32(a[row * k + k0 + q], hi[q], lo[q]);
+    tmem_st8(tmem + lane_addr + a_hi_col + k0, hi);
+    tmem_st8(tmem + lane_addr + a_lo_col + k0, lo);
+  }
+  tmem_st_wait();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  if (tid == 0) {
+    const uint32_t idesc = idesc_tf32(128, n);
+    for (int s = 0; s < k / 8; ++s) {
+      const uint32_t bo = s * 2 * n * 16;
+      const uint64_t bh = desc_kmajor(smem_u32(b_hi) + bo, n * 16, 128);
+      const uint64_t bl = desc_kmajor(smem_u32(b_lo) + bo, n * 16, 128);
+      mma_tf32_ts(tmem, tmem + a_hi_col + 8 * s, bh, idesc, s > 0);
+      if (passes == 3) {
+        mma_tf32_ts(tmem, tmem + a_lo_col + 8 * s, bh, idesc, 1);
+        mma_tf32_ts(tmem, tmem + a_hi_col + 8 * s, bl, idesc, 1);
+      }
+    }
+    mma_commit(&mbar);
+  }
+  mbar_wait(&mbar, 0);
+  fence_after_sync();
+  for (int col = 0; col < n; col += 8) {
+    float v[8];
+    tmem_ld8(tmem + lane_addr + col, v);
+    tmem_ld_wait();
+    for (int j = 0; j < 8; ++j) c[row * n + col + j] = v[j];
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 }  // namespace
+
+extern "C" int dgm_probe_tf32_gemm_ts(const float* a, const float* b, float* c, int n, int k, int passes,
+                                      void* stream) {
+  if (n < 16 || n > 256 || n % 16 || k < 8 || k > 64 || k % 8 || (passes != 1 && passes != 3)) return -1;
+  const size_t smem = (size_t)2 * n * k * sizeof(float);
+  if (cudaFuncSetAttribute(probe_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return -2;
+  probe_ts_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(a, b, c, n, k, passes);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
 
 extern "C" int dgm_probe_tf32_gemm(const float* a, const float* b, float* c, int n, int k, int passes,
                                    void* stream) {

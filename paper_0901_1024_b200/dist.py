@@ -200,7 +200,8 @@ def build_mesh_domain(mesh: Mesh, elem: ReferenceElement, rank: int, world: int,
 class DistributedMaxwellOperator:
     """One rank's share of the operator; halo exchange over torch.distributed (NCCL)."""
 
-    def __init__(self, domain: RankDomain, material: Material = VACUUM, *, dtype=None, device=None):
+    def __init__(self, domain: RankDomain, material: Material = VACUUM, *, dtype=None, device=None,
+                 path: str = "auto"):
         import torch
 
         from .operator import B200MaxwellOperator
@@ -209,7 +210,7 @@ class DistributedMaxwellOperator:
         self.torch = torch
         dtype = torch.float32 if dtype is None else dtype
         self.op = B200MaxwellOperator(domain.elem, material, domain.geo_words, domain.det_j, domain.maps,
-                                      num_ghost=domain.num_ghost, dtype=dtype, device=device)
+                                      num_ghost=domain.num_ghost, dtype=dtype, device=device, path=path)
         self.device = self.op.device
         self.comm_stream = torch.cuda.Stream(self.device)
         rows = 6 * self.op.np_stride

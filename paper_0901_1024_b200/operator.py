@@ -44,6 +44,27 @@ def pack_chunks(mat: np.ndarray, chunks: int, vec: int) -> np.ndarray:
     return np.ascontiguousarray(padded.reshape(rows, chunks, vec).transpose(1, 0, 2))
 
 
+def tc_operand(elem: ReferenceElement, lay) -> np.ndarray:
+    """Constant GEMM operand of the tensor-core path, layout of dgm_desc.tc_operand (include/dgm.h).
+
+    B[n][k] = [D_r | D_s | D_t | LIFT][n][k] with each derivative block tc_npk
+    wide; split into a tf32-exact high part (13 low mantissa bits cleared) and
+    the float32 remainder, so that hi*x + lo*x carries fp32 accuracy.
+    """
+    n_p, nb, npk, steps = elem.num_nodes, lay.tc_nb, lay.tc_npk, lay.tc_steps
+    full = np.zeros((nb, steps * 8))
+    for mu in range(3):
+        full[:n_p, mu * npk:mu * npk + n_p] = elem.diff[mu]
+    full[:n_p, 3 * npk:3 * npk + elem.lift.shape[1]] = elem.lift
+    hi = (full.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    lo = (full - hi.astype(np.float64)).astype(np.float32)
+    parts = np.stack([hi, lo])                                   # (2, nb, K)
+    packed = parts.reshape(2, nb, steps, 2, 4).transpose(2, 0, 3, 1, 4)  # (steps, h, c, n, q)
+    out = np.ascontiguousarray(packed, dtype=np.float32)
+    assert out.size == lay.tc_operand_floats
+    return out
+
+
 def geometry_words(geometry: GeometricFactors) -> np.ndarray:
     """(K, 26) float64 per-element words, layout of dgm_desc.geometry (include/dgm.h)."""
     k = len(geometry.det_jacobians)
@@ -66,7 +87,7 @@ class B200MaxwellOperator:
 
     def __init__(self, elem: ReferenceElement, material: Material, geo_words: np.ndarray,
                  det_j: np.ndarray, maps: FaceMaps, *, num_ghost: int = 0,
-                 dtype: torch.dtype = torch.float32, device=None):
+                 dtype: torch.dtype = torch.float32, device=None, path: str = "auto"):
         if dtype not in _DTYPES:
             raise ValueError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
         if not torch.cuda.is_available():
@@ -102,6 +123,11 @@ class B200MaxwellOperator:
         table = maps.code_table if len(maps.code_table) else np.zeros((1, elem.num_face_nodes), np.uint8)
         self._ptab = dev(table, torch.uint8)
         self._num_codes = int(len(maps.code_table))
+        if path not in _capi.PATHS:
+            raise ValueError(f"path must be one of {sorted(_capi.PATHS)}, got {path!r}")
+        self._tc = None
+        if lay.tc_supported and path != "simt":
+            self._tc = dev(tc_operand(elem, lay), torch.float32)
 
         desc = _capi.Desc(
             order=elem.order, dtype=self._dt_code, num_elements=self.num_elements,
@@ -110,7 +136,8 @@ class B200MaxwellOperator:
             geometry=self._geo.data_ptr(), neighbors=self._nbr.data_ptr(),
             codes=self._code.data_ptr(), face_nodes=self._fmask.data_ptr(),
             code_table=self._ptab.data_ptr(), num_codes=self._num_codes,
-            permittivity=float(material.permittivity), permeability=float(material.permeability))
+            permittivity=float(material.permittivity), permeability=float(material.permeability),
+            tc_operand=self._tc.data_ptr() if self._tc is not None else None, path=_capi.PATHS[path])
         lib = _capi.load()
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
@@ -136,6 +163,12 @@ class B200MaxwellOperator:
     @property
     def order(self) -> int:
         return self.elem.order
+
+    @property
+    def path(self) -> str:
+        """'tensor' (tcgen05 3xTF32 stage kernel) or 'simt' (CUDA-core stage kernel)."""
+        code = self._lib.dgm_plan_path(self._plan)
+        return {_capi.PATH_SIMT: "simt", _capi.PATH_TENSOR: "tensor"}[code]
 
     @property
     def dofs(self) -> int:
@@ -354,14 +387,14 @@ class B200MaxwellOperator:
 
 def build_b200_operator(mesh: Mesh, elem: ReferenceElement, material: Material = VACUUM,
                         connectivity: FaceConnectivity | None = None, *,
-                        dtype: torch.dtype = torch.float32, device=None) -> B200MaxwellOperator:
+                        dtype: torch.dtype = torch.float32, device=None, path: str = "auto") -> B200MaxwellOperator:
     """Drop-in for build_reference_operator (oracle.py:97-141) on one B200."""
     if connectivity is None:
         connectivity = build_connectivity(mesh)
     geometry = compute_geometry(mesh, elem)
     maps = build_face_maps(mesh, elem, connectivity)
     op = B200MaxwellOperator(elem, material, geometry_words(geometry), geometry.det_jacobians, maps,
-                             dtype=dtype, device=device)
+                             dtype=dtype, device=device, path=path)
     op.mesh = mesh
     op.connectivity = connectivity
     op.geometry = geometry

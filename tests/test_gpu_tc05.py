@@ -19,6 +19,7 @@ def probe():
         pytest.skip("no CUDA device")
     lib = ctypes.CDLL(PROBE)
     lib.dgm_probe_tf32_gemm.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 3 + [ctypes.c_void_p]
+    lib.dgm_probe_tf32_gemm_ts.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 3 + [ctypes.c_void_p]
     return lib
 
 
@@ -40,3 +41,22 @@ def test_tf32_and_3xtf32_gemm(probe, n, k):
     assert errs[1] < 5e-3          # plain TF32: ~2^-11 per product
     assert errs[3] < 2e-6          # 3xTF32: fp32-class accuracy
     assert errs[3] < errs[1] / 50
+
+
+@pytest.mark.parametrize("n,k", [(48, 64), (16, 8), (32, 40), (256, 16)])
+def test_tf32_gemm_a_in_tmem(probe, n, k):
+    """TS form: A written to TMEM with tcgen05.st (lane = row), B from smem."""
+    gen = torch.Generator(device="cuda").manual_seed(n + k)
+    a = torch.randn(128, k, device="cuda", generator=gen)
+    b = torch.randn(n, k, device="cuda", generator=gen)
+    want = (a.double() @ b.double().T)
+    errs = {}
+    for passes in (1, 3):
+        c = torch.full((128, n), float("nan"), device="cuda")
+        rc = probe.dgm_probe_tf32_gemm_ts(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, k, passes,
+                                          torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        torch.cuda.synchronize()
+        errs[passes] = ((c.double() - want).norm() / want.norm()).item()
+    print(f"TS n={n} k={k} tf32 {errs[1]:.2e} 3xtf32 {errs[3]:.2e}")
+    assert errs[1] < 5e-3 and errs[3] < 2e-6

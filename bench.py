@@ -181,7 +181,7 @@ def run_b200(args) -> None:
     elem = build_reference_element(args.order)
     if world == 1:
         mesh = generate_box_mesh((1.0, 1.0, 1.0), cells)
-        op = build_b200_operator(mesh, elem, dtype=dtype, device=dev)
+        op = build_b200_operator(mesh, elem, dtype=dtype, device=dev, path=args.path)
         dt = stable_dt(mesh, op.geometry, args.order)
         extent = (1.0, 1.0, 1.0)
         u0_host = CavityMode(1, 1, 1, extent).evaluate(map_nodes(mesh, elem), 0.0)
@@ -194,7 +194,7 @@ def run_b200(args) -> None:
         extent = (float(world), 1.0, 1.0)
         gcells = (cells[0] * world, cells[1], cells[2])
         dom = build_box_domain(extent, gcells, elem, rank, world)
-        runner = DistributedMaxwellOperator(dom, dtype=dtype, device=dev)
+        runner = DistributedMaxwellOperator(dom, dtype=dtype, device=dev, path=args.path)
         op = runner.op
         lo = dom.owned[0] - dom.sub_offset
         own_mesh = Mesh(dom.mesh.vertices, dom.mesh.elements[lo:lo + dom.num_owned])
@@ -247,7 +247,7 @@ def run_b200(args) -> None:
     launch_s = sec / launches
     peaks = _peaks()
     ncu = _ncu_summary()
-    traffic = ncu.get("stage_kernel", {}).get("dram_bytes_per_launch")
+    traffic = ncu.get("tc_stage_kernel" if op.path == "tensor" else "stage_kernel", {}).get("dram_bytes_per_launch")
     fp32_peak_tf = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
 
     # ---- end-to-end through the public API with host buffers ----
@@ -310,7 +310,10 @@ def run_b200(args) -> None:
                    "bytes_per_element_stage": b_alg},
         "roofline": {"bound": "hbm", "achieved": b_alg * k / launch_s / 1e9, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": b_alg * k / launch_s / 1e9 / peaks["hbm_gbs"],
-                     "traffic": traffic, "kernel": f"dgm::stage_kernel<{args.order},{'float' if word == 4 else 'double'},1>",
+                     "traffic": traffic,
+                     "kernel": (f"dgm::tc_stage_kernel<{args.order},1>" if op.path == "tensor" else
+                                f"dgm::stage_kernel<{args.order},{'float' if word == 4 else 'double'},1>"),
+                     "path": op.path,
                      "launch_us": launch_s * 1e6,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "_fallback" not in peaks
                      else "fallback 6.65 TB/s (B200_PROFILING.md)",
@@ -342,6 +345,8 @@ def main(argv=None) -> None:
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--path", choices=("auto", "tensor", "simt"), default="auto",
+                    help="stage kernel: tcgen05 3xTF32 (tensor, N<=4 fp32) or CUDA cores (simt)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -47,7 +47,7 @@ enum {
 };
 
 /* Number of words per element in the geometry array (see dgm_desc). */
-#define DGM_GEO_WORDS 26
+#define DGM_GEO_WORDS 28
 
 /* Device layout of one order/dtype (host and device must agree). */
 typedef struct {
@@ -79,7 +79,7 @@ enum { DGM_PATH_AUTO = 0, DGM_PATH_SIMT = 1, DGM_PATH_TENSOR = 2 };
  *                elem.diff[m][i][c*vec+q] (0 beyond Np)   (refelem.py:378-379)
  *  lift_packed : real[lift_chunks][Np][vec]       lift_packed[c][i][q] =
  *                elem.lift[i][c*vec+q]                     (refelem.py:435-446)
- *  geometry    : real[num_elements_alloc][26] per element:
+ *  geometry    : real[num_elements][28] per element (words 26, 27 are padding):
  *                [0..8]  inv_jacobians row-major (d r_m / d x_n)   (mesh.py:331)
  *                [9]     1 / det_jacobians                         (oracle.py:89)
  *                [10..21] normals[f][3]                            (mesh.py:333-334)

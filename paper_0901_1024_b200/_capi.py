@@ -14,7 +14,7 @@ from dataclasses import dataclass
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdgm.so")
 ABI_VERSION = 2
-GEO_WORDS = 26
+GEO_WORDS = 28
 
 DGM_F32, DGM_F64 = 0, 1
 PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2

@@ -29,7 +29,7 @@
 
 namespace dgm {
 
-constexpr int GEO_WORDS = 26;
+constexpr int GEO_WORDS = 28;  // 26 used + 2 pad: rows are 7 x 16 B, so any row range is TMA-aligned
 
 __host__ __device__ constexpr int np_of(int n) { return (n + 1) * (n + 2) * (n + 3) / 6; }
 __host__ __device__ constexpr int nfp_of(int n) { return (n + 1) * (n + 2) / 2; }

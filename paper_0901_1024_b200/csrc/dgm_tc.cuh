@@ -17,12 +17,14 @@
 // Roles (288 threads, one CTA per SM, persistent over 128-element tiles):
 //   warps 0-7 producers: build A K-steps in registers and tcgen05.st them to
 //     TMEM (warps 0-3: E components from H fields, warps 4-7: H components from
-//     E fields; thread = element row = TMEM lane), copy the B K-step into smem;
-//     the surface flux of a K-step is first computed with a face-node-major
-//     mapping (coalesced neighbor gathers) into smem and transposed;
-//     then the epilogue: TMEM accumulators -> smem -> coalesced LSRK update.
-//   warp 8 lane 0: bulk-copies the u tile (cp.async.bulk, mbarrier tx) and
-//     issues the 18 MMAs of every K-step (A from TMEM, B from smem).
+//     E fields; thread = element row = TMEM lane).  The surface flux of a
+//     K-step is first computed with a face-node-major mapping (coalesced,
+//     batched neighbor gathers) into smem and transposed.  Then the epilogue:
+//     TMEM accumulators -> smem -> coalesced LSRK update.
+//   warp 8 lane 0: cp.async.bulk of the B operand (once per CTA) and of every
+//     tile's u / geometry / connectivity rows (mbarrier tx counts), L2
+//     prefetch of the next tile and of this tile's residual, and issue of the
+//     18 MMAs of every K-step (A from TMEM, B resident in smem).
 // TMEM: [0, 6*NB) accumulators; two A stages of 6 x (8 hi + 8 lo) columns.
 #pragma once
 
@@ -49,18 +51,18 @@ struct TcCfg {
   static constexpr int TMEM_COLS = 512;
   static_assert(A_COL0 + 2 * A_STAGE_COLS <= TMEM_COLS, "TMEM budget");
   static constexpr int SROW = TE + 4;              // flux staging row stride (conflict-free both ways)
-  static constexpr int B_STAGE_BYTES = 2 * 2 * NB * 16;  // hi/lo x 2 chunks x NB rows x 16 B
+  static constexpr int B_STEP_BYTES = 2 * 2 * NB * 16;   // hi/lo x 2 chunks x NB rows x 16 B
   // shared-memory carve-up (bytes)
   static constexpr size_t OFF_U = 0;
   static constexpr size_t OFF_GEO = OFF_U + (size_t)6 * TE * NPG * 4;
   static constexpr size_t OFF_NBR = OFF_GEO + (size_t)TE * GEO_WORDS * 4;
   static constexpr size_t OFF_CODE = OFF_NBR + (size_t)TE * 4 * 4;
-  static constexpr size_t STAGE_BYTES = (size_t)2 * 6 * 8 * SROW * 4 > (size_t)2 * TE * NPG * 4
-                                            ? (size_t)2 * 6 * 8 * SROW * 4
-                                            : (size_t)2 * TE * NPG * 4;
-  static constexpr size_t OFF_STAGE = OFF_CODE + (size_t)TE * 4 * 4;
-  static constexpr size_t OFF_B = OFF_STAGE + STAGE_BYTES;
-  static constexpr size_t OFF_BAR = OFF_B + (size_t)2 * B_STAGE_BYTES;
+  static constexpr size_t OFF_B = OFF_CODE + (size_t)TE * 4 * 4;
+  static constexpr size_t STAGE_BYTES = (size_t)6 * 8 * SROW * 4 > (size_t)TE * NPG * 4
+                                            ? (size_t)6 * 8 * SROW * 4
+                                            : (size_t)TE * NPG * 4;
+  static constexpr size_t OFF_STAGE = OFF_B + (size_t)KS * B_STEP_BYTES;
+  static constexpr size_t OFF_BAR = OFF_STAGE + STAGE_BYTES;
   static constexpr size_t OFF_FMASK = OFF_BAR + 64;
   static constexpr size_t OFF_PTAB = OFF_FMASK + (4 * NFP + 15) / 16 * 16;
   static constexpr size_t SMEM_FIXED = OFF_PTAB;   // + ncodes * NFP
@@ -86,14 +88,15 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
   float* s_geo = reinterpret_cast<float*>(smem + T::OFF_GEO);
   int* s_nbr = reinterpret_cast<int*>(smem + T::OFF_NBR);
   int* s_code = reinterpret_cast<int*>(smem + T::OFF_CODE);
-  float* s_stage = reinterpret_cast<float*>(smem + T::OFF_STAGE);
   unsigned char* s_b = smem + T::OFF_B;
+  float* s_stage = reinterpret_cast<float*>(smem + T::OFF_STAGE);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
   uint64_t* full = bar + 0;      // [2] producers -> MMA
   uint64_t* empty = bar + 2;     // [2] MMA commit -> producers
-  uint64_t* load_full = bar + 4; // u tile landed
+  uint64_t* load_full = bar + 4; // tile rows landed
   uint64_t* acc_full = bar + 5;  // accumulators final
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 6);
+  uint64_t* b_full = bar + 6;    // resident B operand landed
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 7);
   uint8_t* s_fmask = smem + T::OFF_FMASK;
   uint8_t* s_ptab = smem + T::OFF_PTAB;
 
@@ -108,6 +111,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     mbar_init(&empty[1], 1);
     mbar_init(load_full, 1);
     mbar_init(acc_full, 1);
+    mbar_init(b_full, 1);
     mbar_init_fence();
   }
   for (int c = tid; c < 4 * NFP; c += blockDim.x) s_fmask[c] = a.fmask[c];
@@ -116,6 +120,12 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = *s_tmem;
+
+  if (tid == T::PROD) {  // resident B operand: once per CTA
+    constexpr uint32_t bbytes = (uint32_t)(KS * T::B_STEP_BYTES);
+    mbar_expect_tx(b_full, bbytes);
+    bulk_g2s(s_b, args.bpack, bbytes, b_full);
+  }
 
   // per-thread role constants
   const int quad = warp & 3;           // TMEM lane quadrant
@@ -131,26 +141,36 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
   for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
     const int64_t e0 = a.e_begin + (int64_t)tile * TE;
     const int nv = (int)min((int64_t)TE, a.e_end - e0);
-    __syncthreads();  // previous tile's epilogue is done with s_u / s_stage
+    __syncthreads();  // previous tile's epilogue is done with s_u / s_stage / s_geo
 
     if (warp == 8) {
       if (lane == 0) {
         const uint32_t rowbytes = (uint32_t)nv * NPG * 4;
-        mbar_expect_tx(load_full, 6 * rowbytes);
+        const uint32_t geobytes = (uint32_t)nv * GEO_WORDS * 4, conbytes = (uint32_t)nv * 16;
+        mbar_expect_tx(load_full, 6 * rowbytes + geobytes + 2 * conbytes);
         for (int f = 0; f < 6; ++f)
           bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowbytes, load_full);
+        bulk_g2s(s_geo, a.geo + e0 * GEO_WORDS, geobytes, load_full);
+        bulk_g2s(s_nbr, a.nbr + e0 * 4, conbytes, load_full);
+        bulk_g2s(s_code, a.code + e0 * 4, conbytes, load_full);
+        if (MODE == MODE_LSRK && !a.a_zero)
+          for (int f = 0; f < 6; ++f) prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rowbytes);
         const int nt = tile + gridDim.x;  // warm L2 with the next tile of this CTA
         if (nt < args.num_tiles) {
           const int64_t n0 = a.e_begin + (int64_t)nt * TE;
-          const uint32_t nb = (uint32_t)min((int64_t)TE, a.e_end - n0) * NPG * 4;
-          for (int f = 0; f < 6; ++f) prefetch_l2(a.u + (int64_t)f * fstride + n0 * NPG, nb);
+          const uint32_t nn = (uint32_t)min((int64_t)TE, a.e_end - n0);
+          for (int f = 0; f < 6; ++f) prefetch_l2(a.u + (int64_t)f * fstride + n0 * NPG, nn * NPG * 4);
+          prefetch_l2(a.geo + n0 * GEO_WORDS, nn * GEO_WORDS * 4);
+          prefetch_l2(a.nbr + n0 * 4, nn * 16);
+          prefetch_l2(a.code + n0 * 4, nn * 16);
         }
+        if (it == 0) mbar_wait(b_full, 0);
         // ---------------- MMA issuer ----------------
         for (int s = 0; s < KS; ++s, ++mstep) {
           const int slot = mstep & 1;
           mbar_wait(&full[slot], (mstep >> 1) & 1);
           fence_after_sync();
-          const uint32_t bh = smem_u32(s_b + slot * T::B_STAGE_BYTES);
+          const uint32_t bh = smem_u32(s_b + s * T::B_STEP_BYTES);
           const uint64_t dbh = desc_kmajor(bh, NB * 16, 128);
           const uint64_t dbl = desc_kmajor(bh + 2 * NB * 16, NB * 16, 128);
 #pragma unroll
@@ -170,90 +190,88 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     }
 
     // ================= producers (warps 0-7) =================
-    // per-tile small data: geometry rows, neighbor ids, codes
-    for (int c = tid; c < TE * GEO_WORDS; c += T::PROD)
-      s_geo[c] = (c < nv * GEO_WORDS) ? a.geo[e0 * GEO_WORDS + c] : 0.0f;
-    for (int c = tid; c < TE * 4; c += T::PROD) {
-      const bool ok = c < nv * 4;
-      s_nbr[c] = ok ? a.nbr[e0 * 4 + c] : 0;
-      s_code[c] = ok ? a.code[e0 * 4 + c] : -1;
-    }
     mbar_wait(load_full, it & 1);
-    named_sync(1, T::PROD);
 
     // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu
+    const bool row_ok = row < nv;
     float prx[9];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) prx[q] = s_geo[row * GEO_WORDS + q] * inv_m;
-    const bool row_ok = row < nv;
+    for (int q = 0; q < 9; ++q) prx[q] = row_ok ? s_geo[row * GEO_WORDS + q] * inv_m : 0.f;
 
     for (int s = 0; s < KS; ++s, ++pstep) {
       const int slot = pstep & 1;
-      float* stg = s_stage + (s & 1) * (6 * 8 * SROW);
       const int k0 = s * 8;
-      // ---- surface flux of this step's face nodes, face-node-major mapping ----
+      // ---- surface flux of this step's face nodes: face-node-major mapping ----
       if (k0 + 8 > KV && k0 < KT) {
-#pragma unroll 1
-        for (int item = tid; item < TE * 8; item += T::PROD) {
+        named_sync(1, T::PROD);  // every thread finished reading the staging of the previous step
+        constexpr int ITEMS = TE * 8 / T::PROD;  // 4 (row, face node) items per thread
+        float um[ITEMS][6], up[ITEMS][6];
+        float nrm[ITEMS][3], sc[ITEMS];
+        bool pec[ITEMS], live[ITEMS];
+        int rr[ITEMS], qq_[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int item = tid + i * T::PROD;
           const int r = item >> 3, qq = item & 7;
           const int q = k0 + qq - KV;
-          if (q < 0 || q >= T::NF4) continue;
-          float out[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          if (r < nv) {
-            const int face = q / NFP, node = q - face * NFP;
-            const int im = s_fmask[face * NFP + node];
-            float um[6], up[6];
+          rr[i] = r;
+          qq_[i] = qq;
+          live[i] = (q >= 0 && q < T::NF4 && r < nv);
+          const int qc = live[i] ? q : 0;
+          const int face = qc / NFP, node = qc - face * NFP;
+          const int im = s_fmask[face * NFP + node];
+          const float* gk = s_geo + r * GEO_WORDS;
+          nrm[i][0] = gk[10 + 3 * face];
+          nrm[i][1] = gk[11 + 3 * face];
+          nrm[i][2] = gk[12 + 3 * face];
+          sc[i] = gk[22 + face] * gk[9];
+          const int code = live[i] ? s_code[r * 4 + face] : -1;
+          pec[i] = code < 0;
 #pragma unroll
-            for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + r) * NPG + im];
-            const float* gk = s_geo + r * GEO_WORDS;
-            const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
-            const int code = s_code[r * 4 + face];
-            if (code < 0) {
-              const float nde = nx * um[0] + ny * um[1] + nz * um[2];
-              const float ndh = nx * um[3] + ny * um[4] + nz * um[5];
-              up[0] = -um[0] + 2.f * nde * nx;
-              up[1] = -um[1] + 2.f * nde * ny;
-              up[2] = -um[2] + 2.f * nde * nz;
-              up[3] = um[3] - 2.f * ndh * nx;
-              up[4] = um[4] - 2.f * ndh * ny;
-              up[5] = um[5] - 2.f * ndh * nz;
+          for (int f = 0; f < 6; ++f) um[i][f] = s_u[(f * TE + r) * NPG + im];
+          // u+ source: own row (PEC, mirrored below), tile row in smem, or a global row
+          const float* src = s_u + r * NPG + im;
+          int64_t fs = TE * NPG;
+          if (!pec[i]) {
+            const int nb = s_nbr[r * 4 + face];
+            const int jn = s_ptab[code * NFP + node];
+            const int64_t loc = (int64_t)nb - e0;
+            if (loc >= 0 && loc < nv) {
+              src = s_u + (int)loc * NPG + jn;
             } else {
-              const int nb = s_nbr[r * 4 + face];
-              const int jn = s_ptab[code * NFP + node];
-              const int64_t loc = (int64_t)nb - e0;
-              if (loc >= 0 && loc < nv) {
-#pragma unroll
-                for (int f = 0; f < 6; ++f) up[f] = s_u[(f * TE + (int)loc) * NPG + jn];
-              } else {
-                const float* p = a.u + (int64_t)nb * NPG + jn;
-#pragma unroll
-                for (int f = 0; f < 6; ++f) up[f] = __ldg(p + f * fstride);
-              }
+              src = a.u + (int64_t)nb * NPG + jn;
+              fs = fstride;
             }
-            upwind(um, up, nx, ny, nz, a, out);
-            const float sc = gk[22 + face] * gk[9];
-#pragma unroll
-            for (int f = 0; f < 3; ++f) out[f] *= sc * a.inv_eps;
-#pragma unroll
-            for (int f = 3; f < 6; ++f) out[f] *= sc * a.inv_mu;
           }
 #pragma unroll
-          for (int c = 0; c < 6; ++c) stg[(c * 8 + qq) * SROW + r] = out[c];
+          for (int f = 0; f < 6; ++f) up[i][f] = src[f * fs];  // generic loads, all in flight together
+        }
+        float* stg = s_stage;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const float nx = nrm[i][0], ny = nrm[i][1], nz = nrm[i][2];
+          if (pec[i]) {  // PEC mirror (maxwell.py:117-132)
+            const float nde = nx * um[i][0] + ny * um[i][1] + nz * um[i][2];
+            const float ndh = nx * um[i][3] + ny * um[i][4] + nz * um[i][5];
+            up[i][0] = -um[i][0] + 2.f * nde * nx;
+            up[i][1] = -um[i][1] + 2.f * nde * ny;
+            up[i][2] = -um[i][2] + 2.f * nde * nz;
+            up[i][3] = um[i][3] - 2.f * ndh * nx;
+            up[i][4] = um[i][4] - 2.f * ndh * ny;
+            up[i][5] = um[i][5] - 2.f * ndh * nz;
+          }
+          float out[6];
+          upwind(um[i], up[i], nx, ny, nz, a, out);
+          const float se = live[i] ? sc[i] * a.inv_eps : 0.f, sh = live[i] ? sc[i] * a.inv_mu : 0.f;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) stg[(c * 8 + qq_[i]) * SROW + rr[i]] = out[c] * se;
+#pragma unroll
+          for (int c = 3; c < 6; ++c) stg[(c * 8 + qq_[i]) * SROW + rr[i]] = out[c] * sh;
         }
         named_sync(1, T::PROD);
       }
 
-      // ---- B K-step into smem and A K-step into TMEM (thread-per-row) ----
-      mbar_wait(&empty[slot], ((pstep >> 1) & 1) ^ 1);
-      fence_after_sync();
-      {
-        constexpr int BV = T::B_STAGE_BYTES / 16;
-        if (tid < BV) {
-          const float4* src = reinterpret_cast<const float4*>(args.bpack) + (size_t)s * BV + tid;
-          reinterpret_cast<float4*>(s_b + slot * T::B_STAGE_BYTES)[tid] = __ldg(src);
-          fence_async_smem();
-        }
-      }
+      // ---- A K-step into TMEM (thread-per-row) ----
       float v[3][8];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -262,9 +280,9 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
           const int mu = k / NPK, j0 = k - mu * NPK;
           const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
           const int fb = grp == 0 ? 3 : 0;  // E comps read H fields and vice versa
-          float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + 0) * TE + row) * NPG + j0);
-          float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + 1) * TE + row) * NPG + j0);
-          float4 z = *reinterpret_cast<const float4*>(s_u + ((fb + 2) * TE + row) * NPG + j0);
+          const float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + 0) * TE + row) * NPG + j0);
+          const float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + 1) * TE + row) * NPG + j0);
+          const float4 z = *reinterpret_cast<const float4*>(s_u + ((fb + 2) * TE + row) * NPG + j0);
           const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w}, zs[4] = {z.x, z.y, z.z, z.w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -282,7 +300,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
 #pragma unroll
           for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) v[c][4 * h + q] = stg[((3 * grp + c) * 8 + 4 * h + q) * SROW + row];
+            for (int c = 0; c < 3; ++c) v[c][4 * h + q] = s_stage[((3 * grp + c) * 8 + 4 * h + q) * SROW + row];
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
@@ -290,17 +308,18 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
             for (int c = 0; c < 3; ++c) v[c][4 * h + q] = 0.f;
         }
       }
+      float hi[3][8], lo[3][8];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) split_tf32(row_ok ? v[c][q] : 0.f, hi[c][q], lo[c][q]);
+      mbar_wait(&empty[slot], ((pstep >> 1) & 1) ^ 1);
+      fence_after_sync();
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        float hi[8], lo[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float x = row_ok ? v[c][q] : 0.f;
-          split_tf32(x, hi[q], lo[q]);
-        }
         const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + (3 * grp + c) * 16;
-        tmem_st8(tmem + lane_addr + col, hi);
-        tmem_st8(tmem + lane_addr + col + 8, lo);
+        tmem_st8(tmem + lane_addr + col, hi[c]);
+        tmem_st8(tmem + lane_addr + col + 8, lo[c]);
       }
       tmem_st_wait();
       fence_before_sync();
@@ -311,12 +330,14 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     // ================= epilogue: accumulators -> LSRK update =================
     mbar_wait(acc_full, it & 1);
     fence_after_sync();
-    float* es = s_stage;  // [2][TE][NPG]
+    named_sync(1, T::PROD);  // staging free (last flux step's reads are done)
+    float* es = s_stage;     // [TE][NPG], one component at a time
+    constexpr int RV = NPG / 4;
+    constexpr int PER = (TE * RV + T::PROD - 1) / T::PROD;
 #pragma unroll 1
-    for (int round = 0; round < 3; ++round) {
-      const int comp = 2 * round + grp;
-      {
-        float* dst = es + (grp * TE + row) * NPG;
+    for (int comp = 0; comp < 6; ++comp) {
+      if (grp == (comp & 1)) {  // the group whose quadrant-warps hold this component's rows
+        float* dst = es + row * NPG;
 #pragma unroll
         for (int c0 = 0; c0 < NB; c0 += 8) {
           float r8[8];
@@ -337,32 +358,41 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
         }
       }
       named_sync(1, T::PROD);
-      constexpr int RV = NPG / 4;
       const int nvec = nv * RV;
-#pragma unroll 1
-      for (int g2 = 0; g2 < 2; ++g2) {
-        const int f = 2 * round + g2;
-        const int64_t gbase = ((int64_t)f * a.kf + e0) * NPG;
-        const float4* rs = reinterpret_cast<const float4*>(es + g2 * TE * NPG);
-        const float4* us = reinterpret_cast<const float4*>(s_u + f * TE * NPG);
-        for (int c = tid; c < nvec; c += T::PROD) {
-          const float4 rh = rs[c];
-          const int64_t go = gbase + (int64_t)c * 4;
-          if (MODE == MODE_RHS) {
-            *reinterpret_cast<float4*>(a.out + go) = rh;
-          } else {
+      const int64_t gbase = ((int64_t)comp * a.kf + e0) * NPG;
+      const float4* rs = reinterpret_cast<const float4*>(es);
+      const float4* us = reinterpret_cast<const float4*>(s_u + comp * TE * NPG);
+      if (MODE == MODE_RHS) {
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+          const int c = tid + p * T::PROD;
+          if (c < nvec) *reinterpret_cast<float4*>(a.out + gbase + (int64_t)c * 4) = rs[c];
+        }
+      } else {
+        float4 ro[PER];
+        if (!a.a_zero) {
+#pragma unroll
+          for (int p = 0; p < PER; ++p) {  // all residual loads in flight before any use
+            const int c = tid + p * T::PROD;
+            ro[p] = c < nvec ? __ldcs(reinterpret_cast<const float4*>(a.res + gbase) + c) : make_float4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < PER; ++p) {
+          const int c = tid + p * T::PROD;
+          if (c < nvec) {
+            const float4 rh = rs[c];
             float4 r;
             if (a.a_zero) {
               r = make_float4(a.dt * rh.x, a.dt * rh.y, a.dt * rh.z, a.dt * rh.w);
             } else {
-              const float4 ro = *reinterpret_cast<const float4*>(a.res + go);
-              r = make_float4(a.a * ro.x + a.dt * rh.x, a.a * ro.y + a.dt * rh.y, a.a * ro.z + a.dt * rh.z,
-                              a.a * ro.w + a.dt * rh.w);
+              r = make_float4(a.a * ro[p].x + a.dt * rh.x, a.a * ro[p].y + a.dt * rh.y,
+                              a.a * ro[p].z + a.dt * rh.z, a.a * ro[p].w + a.dt * rh.w);
             }
-            *reinterpret_cast<float4*>(a.res + go) = r;
+            __stcs(reinterpret_cast<float4*>(a.res + gbase) + c, r);
             const float4 uo = us[c];
-            *reinterpret_cast<float4*>(a.u_out + go) =
-                make_float4(uo.x + a.b * r.x, uo.y + a.b * r.y, uo.z + a.b * r.z, uo.w + a.b * r.w);
+            __stcs(reinterpret_cast<float4*>(a.u_out + gbase) + c,
+                   make_float4(uo.x + a.b * r.x, uo.y + a.b * r.y, uo.z + a.b * r.z, uo.w + a.b * r.w));
           }
         }
       }

@@ -66,9 +66,9 @@ def tc_operand(elem: ReferenceElement, lay) -> np.ndarray:
 
 
 def geometry_words(geometry: GeometricFactors) -> np.ndarray:
-    """(K, 26) float64 per-element words, layout of dgm_desc.geometry (include/dgm.h)."""
+    """(K, 28) float64 per-element words, layout of dgm_desc.geometry (include/dgm.h)."""
     k = len(geometry.det_jacobians)
-    g = np.empty((k, _capi.GEO_WORDS))
+    g = np.zeros((k, _capi.GEO_WORDS))
     g[:, 0:9] = geometry.inv_jacobians.reshape(k, 9)
     g[:, 9] = 1.0 / geometry.det_jacobians
     g[:, 10:22] = geometry.normals.reshape(k, 12)

@@ -67,6 +67,8 @@ typedef struct {
   int32_t tc_nb;            /* MMA N: Np rounded up to 16                     */
   int32_t tc_steps;         /* K steps of 8 (K = 3*tc_npk + 4*Nfp, padded)     */
   int32_t tc_npk;           /* K extent of one derivative block (Np up to 4)  */
+  int32_t tc_kv;            /* K offset of the first face block (3*npk up to 8) */
+  int32_t tc_nfpk;          /* K extent of one face block (Nfp up to 8)       */
   int64_t tc_operand_floats;/* size of dgm_desc.tc_operand in floats          */
 } dgm_layout_info;
 
@@ -93,8 +95,9 @@ enum { DGM_PATH_AUTO = 0, DGM_PATH_SIMT = 1, DGM_PATH_TENSOR = 2 };
  *  code_table  : uint8[num_codes][Nfp]    vmap_plus rows minus neighbor*Np
  *                (oracle.py:116-123)
  *  tc_operand  : float[tc_steps][2][2][tc_nb][4], the constant GEMM operand
- *                B[n][k] = [D_r | D_s | D_t | LIFT][n][k] (derivative blocks
- *                tc_npk wide, zero padded) split into tf32 hi / exact lo parts:
+ *                B[n][k]: D_mu[n][j] at k = mu*tc_npk + j, LIFT[n][f*Nfp + i]
+ *                at k = tc_kv + f*tc_nfpk + i, zero elsewhere; split into a
+ *                tf32 hi part and the exact fp32 remainder:
  *                tc_operand[s][h][c][n][q] = part_h(B[n][8s + 4c + q]).
  *                NULL disables the tensor-core path.
  *  path        : DGM_PATH_AUTO (tensor cores when available), _SIMT or _TENSOR.

@@ -34,7 +34,7 @@ class LayoutInfo(ctypes.Structure):
                 ("tile_elements", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("smem_bytes_fixed", ctypes.c_int64), ("tc_supported", ctypes.c_int32),
                 ("tc_nb", ctypes.c_int32), ("tc_steps", ctypes.c_int32), ("tc_npk", ctypes.c_int32),
-                ("tc_operand_floats", ctypes.c_int64)]
+                ("tc_kv", ctypes.c_int32), ("tc_nfpk", ctypes.c_int32), ("tc_operand_floats", ctypes.c_int64)]
 
 
 class Desc(ctypes.Structure):
@@ -114,6 +114,8 @@ class Layout:
     tc_nb: int
     tc_steps: int
     tc_npk: int
+    tc_kv: int
+    tc_nfpk: int
     tc_operand_floats: int
 
 

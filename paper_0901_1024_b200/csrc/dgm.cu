@@ -75,7 +75,7 @@ namespace {
 template <int N, typename T>
 struct TcInfo {
   static constexpr bool supported = false;
-  static constexpr int nb = 0, steps = 0, npk = 0;
+  static constexpr int nb = 0, steps = 0, npk = 0, kv = 0, nfpk = 0;
   static constexpr int64_t floats = 0;
 };
 #define DGM_TC_INFO(n)                                                   \
@@ -84,6 +84,7 @@ struct TcInfo {
     static constexpr bool supported = true;                              \
     static constexpr int nb = dgm::TcCfg<n>::NB, steps = dgm::TcCfg<n>::KS; \
     static constexpr int npk = dgm::TcCfg<n>::NPK;                       \
+    static constexpr int kv = dgm::TcCfg<n>::KV, nfpk = dgm::TcCfg<n>::NFPK; \
     static constexpr int64_t floats = (int64_t)dgm::TcCfg<n>::B_FLOATS;  \
   };
 DGM_TC_INFO(1)
@@ -119,6 +120,8 @@ int dgm_layout(int32_t order, int32_t dtype, dgm_layout_info* out) {
     out->tc_nb = TI::nb;
     out->tc_steps = TI::steps;
     out->tc_npk = TI::npk;
+    out->tc_kv = TI::kv;
+    out->tc_nfpk = TI::nfpk;
     out->tc_operand_floats = TI::floats;
     return DGM_OK;
   });

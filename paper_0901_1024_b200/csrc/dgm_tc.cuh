@@ -8,20 +8,21 @@
 //   f^(c)    = upwind_bracket_c * face_jacobian / det_J / (eps|mu)
 //
 // because d/dx_nu u = sum_mu rx[mu][nu] D_mu u and rx is constant per element.
-// So with A[e][k] = [w_0 | w_1 | w_2 | f] (K = 3*NPK + 4*Nfp) and the constant
-// B[n][k] = [D_0 | D_1 | D_2 | LIFT] (rows n = output node), one tcgen05.mma
-// chain per component computes the full RHS of 128 elements (M = 128 lanes
-// of TMEM, one element per lane).  fp32 accuracy comes from 3xTF32
-// (A_hi B_hi + A_lo B_hi + A_hi B_lo) with exact hi/lo splits.
+// So with A[e][k] = [w_0 | w_1 | w_2 | pad | f_face0 | .. | f_face3] and the
+// constant B[n][k] = [D_0 | D_1 | D_2 | 0 | LIFT_face0 | .. ] (rows n = output
+// node; every face block padded to NFPK = ceil8(Nfp) so a flux K-step never
+// straddles two faces), one tcgen05.mma chain per component computes the full
+// RHS of 128 elements (M = 128 TMEM lanes, one element per lane).  fp32
+// accuracy comes from 3xTF32 (A_hi B_hi + A_lo B_hi + A_hi B_lo), exact splits.
 //
-// Roles (288 threads, one CTA per SM, persistent over 128-element tiles):
-//   warps 0-7 producers: build A K-steps in registers and tcgen05.st them to
-//     TMEM (warps 0-3: E components from H fields, warps 4-7: H components from
-//     E fields; thread = element row = TMEM lane).  The surface flux of a
-//     K-step is first computed with a face-node-major mapping (coalesced,
-//     batched neighbor gathers) into smem and transposed.  Then the epilogue:
-//     TMEM accumulators -> smem -> coalesced LSRK update.
-//   warp 8 lane 0: cp.async.bulk of the B operand (once per CTA) and of every
+// Roles (544 threads, one CTA per SM, persistent over 128-element tiles):
+//   warps 0-15 producers.  Surface flux of a K-step: face-node-major mapping
+//     (8 lanes per element row, coalesced neighbor gathers) into smem.  A
+//     K-step: thread-per-row (row = TMEM lane); warp w serves lane quadrant
+//     w%4, component group (w/8: E components from H fields, or H components
+//     from E fields) and K half ((w/4)%2); tcgen05.st of hi and lo parts.
+//     Epilogue: TMEM accumulators -> smem -> coalesced LSRK update.
+//   warp 16 lane 0: cp.async.bulk of the B operand (once per CTA) and of each
 //     tile's u / geometry / connectivity rows (mbarrier tx counts), L2
 //     prefetch of the next tile and of this tile's residual, and issue of the
 //     18 MMAs of every K-step (A from TMEM, B resident in smem).
@@ -38,12 +39,14 @@ struct TcCfg {
   using C = Cfg<N, float>;
   static constexpr int NP = C::NP, NFP = C::NFP, NF4 = C::NF4, NPG = C::NPG;
   static constexpr int NPK = (NP + 3) / 4 * 4;     // K extent of one volume block
+  static constexpr int NFPK = (NFP + 7) / 8 * 8;   // K extent of one face block
   static constexpr int NB = (NP + 15) / 16 * 16;   // MMA N (M=128, A in TMEM: N % 16 == 0)
-  static constexpr int KV = 3 * NPK;               // volume part of K
-  static constexpr int KT = KV + NF4;
-  static constexpr int KS = (KT + 7) / 8;          // K steps (one kind::tf32 MMA each)
+  static constexpr int KV = (3 * NPK + 7) / 8 * 8; // volume part of K, padded to a K step
+  static constexpr int KT = KV + 4 * NFPK;
+  static constexpr int KS = KT / 8;                // K steps (one kind::tf32 MMA each)
   static constexpr int TE = 128;
-  static constexpr int PROD = 256;                 // producer threads (8 warps)
+  static constexpr int PWARPS = 16;
+  static constexpr int PROD = 32 * PWARPS;         // producer threads
   static constexpr int THREADS = PROD + 32;
   static constexpr int ACC_COLS = 6 * NB;
   static constexpr int A_COL0 = (ACC_COLS + 31) / 32 * 32;
@@ -79,8 +82,8 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const TcArgs args) {
   using T = TcCfg<N>;
   using namespace tc;
-  constexpr int TE = T::TE, NPG = T::NPG, NP = T::NP, NFP = T::NFP, NB = T::NB;
-  constexpr int KS = T::KS, KV = T::KV, KT = T::KT, NPK = T::NPK, SROW = T::SROW;
+  constexpr int TE = T::TE, NPG = T::NPG, NP = T::NP, NFP = T::NFP, NB = T::NB, NFPK = T::NFPK;
+  constexpr int KS = T::KS, KV = T::KV, NPK = T::NPK, SROW = T::SROW, PROD = T::PROD;
   const StageArgs<float>& a = args.s;
 
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -104,9 +107,9 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
   const int64_t fstride = a.kf * NPG;
 
   if (warp == 0) tmem_alloc(s_tmem, T::TMEM_COLS);
-  if (tid == T::PROD) {
-    mbar_init(&full[0], 8);
-    mbar_init(&full[1], 8);
+  if (tid == PROD) {
+    mbar_init(&full[0], T::PWARPS);
+    mbar_init(&full[1], T::PWARPS);
     mbar_init(&empty[0], 1);
     mbar_init(&empty[1], 1);
     mbar_init(load_full, 1);
@@ -121,16 +124,17 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
   fence_after_sync();
   const uint32_t tmem = *s_tmem;
 
-  if (tid == T::PROD) {  // resident B operand: once per CTA
+  if (tid == PROD) {  // resident B operand: once per CTA
     constexpr uint32_t bbytes = (uint32_t)(KS * T::B_STEP_BYTES);
     mbar_expect_tx(b_full, bbytes);
     bulk_g2s(s_b, args.bpack, bbytes, b_full);
   }
 
-  // per-thread role constants
-  const int quad = warp & 3;           // TMEM lane quadrant
-  const int grp = (warp >> 2) & 1;     // 0: E components (from H fields), 1: H components (from E fields)
-  const int row = quad * 32 + lane;    // element row owned in thread-per-row phases
+  // per-thread role constants (thread-per-row phases)
+  const int quad = warp & 3;               // TMEM lane quadrant
+  const int khalf = (warp >> 2) & 1;       // which 4 of a K step's 8 columns
+  const int grp = (warp >> 3) & 1;         // 0: E components (from H fields), 1: H components (from E fields)
+  const int row = quad * 32 + lane;        // element row = TMEM lane
   const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
   const float inv_m = grp == 0 ? a.inv_eps : a.inv_mu;
   const uint32_t idesc = idesc_tf32(128, NB);
@@ -143,7 +147,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     const int nv = (int)min((int64_t)TE, a.e_end - e0);
     __syncthreads();  // previous tile's epilogue is done with s_u / s_stage / s_geo
 
-    if (warp == 8) {
+    if (warp == T::PWARPS) {
       if (lane == 0) {
         const uint32_t rowbytes = (uint32_t)nv * NPG * 4;
         const uint32_t geobytes = (uint32_t)nv * GEO_WORDS * 4, conbytes = (uint32_t)nv * 16;
@@ -189,7 +193,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
       continue;
     }
 
-    // ================= producers (warps 0-7) =================
+    // ================= producers =================
     mbar_wait(load_full, it & 1);
 
     // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu
@@ -201,38 +205,26 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     for (int s = 0; s < KS; ++s, ++pstep) {
       const int slot = pstep & 1;
       const int k0 = s * 8;
-      // ---- surface flux of this step's face nodes: face-node-major mapping ----
-      if (k0 + 8 > KV && k0 < KT) {
-        named_sync(1, T::PROD);  // every thread finished reading the staging of the previous step
-        constexpr int ITEMS = TE * 8 / T::PROD;  // 4 (row, face node) items per thread
+      // ---- surface flux of this step (one face, 8 face nodes): face-node-major mapping ----
+      if (k0 >= KV) {
+        named_sync(1, PROD);  // every thread finished reading the staging of the previous step
+        const int face = (k0 - KV) / NFPK;
+        const int node0 = (k0 - KV) - face * NFPK;
+        constexpr int ITEMS = TE * 8 / PROD;  // (row, face node) items per thread
         float um[ITEMS][6], up[ITEMS][6];
-        float nrm[ITEMS][3], sc[ITEMS];
-        bool pec[ITEMS], live[ITEMS];
-        int rr[ITEMS], qq_[ITEMS];
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-          const int item = tid + i * T::PROD;
-          const int r = item >> 3, qq = item & 7;
-          const int q = k0 + qq - KV;
-          rr[i] = r;
-          qq_[i] = qq;
-          live[i] = (q >= 0 && q < T::NF4 && r < nv);
-          const int qc = live[i] ? q : 0;
-          const int face = qc / NFP, node = qc - face * NFP;
-          const int im = s_fmask[face * NFP + node];
-          const float* gk = s_geo + r * GEO_WORDS;
-          nrm[i][0] = gk[10 + 3 * face];
-          nrm[i][1] = gk[11 + 3 * face];
-          nrm[i][2] = gk[12 + 3 * face];
-          sc[i] = gk[22 + face] * gk[9];
-          const int code = live[i] ? s_code[r * 4 + face] : -1;
-          pec[i] = code < 0;
+          const int item = tid + i * PROD;
+          const int r = item >> 3, node = node0 + (item & 7);
+          const bool live = node < NFP && r < nv;
+          const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
 #pragma unroll
           for (int f = 0; f < 6; ++f) um[i][f] = s_u[(f * TE + r) * NPG + im];
-          // u+ source: own row (PEC, mirrored below), tile row in smem, or a global row
+          // u+ source: own row (PEC mirror below), tile row in smem, or a global row
           const float* src = s_u + r * NPG + im;
           int64_t fs = TE * NPG;
-          if (!pec[i]) {
+          const int code = live ? s_code[r * 4 + face] : -1;
+          if (code >= 0) {
             const int nb = s_nbr[r * 4 + face];
             const int jn = s_ptab[code * NFP + node];
             const int64_t loc = (int64_t)nb - e0;
@@ -246,11 +238,14 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
 #pragma unroll
           for (int f = 0; f < 6; ++f) up[i][f] = src[f * fs];  // generic loads, all in flight together
         }
-        float* stg = s_stage;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-          const float nx = nrm[i][0], ny = nrm[i][1], nz = nrm[i][2];
-          if (pec[i]) {  // PEC mirror (maxwell.py:117-132)
+          const int item = tid + i * PROD;
+          const int r = item >> 3, qq = item & 7, node = node0 + qq;
+          const bool live = node < NFP && r < nv;
+          const float* gk = s_geo + r * GEO_WORDS;
+          const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
+          if (live && s_code[r * 4 + face] < 0) {  // PEC mirror (maxwell.py:117-132)
             const float nde = nx * um[i][0] + ny * um[i][1] + nz * um[i][2];
             const float ndh = nx * um[i][3] + ny * um[i][4] + nz * um[i][5];
             up[i][0] = -um[i][0] + 2.f * nde * nx;
@@ -262,21 +257,21 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
           }
           float out[6];
           upwind(um[i], up[i], nx, ny, nz, a, out);
-          const float se = live[i] ? sc[i] * a.inv_eps : 0.f, sh = live[i] ? sc[i] * a.inv_mu : 0.f;
+          const float sc = live ? gk[22 + face] * gk[9] : 0.f;
+          const float se = sc * a.inv_eps, sh = sc * a.inv_mu;
 #pragma unroll
-          for (int c = 0; c < 3; ++c) stg[(c * 8 + qq_[i]) * SROW + rr[i]] = out[c] * se;
+          for (int c = 0; c < 3; ++c) s_stage[(c * 8 + qq) * SROW + r] = out[c] * se;
 #pragma unroll
-          for (int c = 3; c < 6; ++c) stg[(c * 8 + qq_[i]) * SROW + rr[i]] = out[c] * sh;
+          for (int c = 3; c < 6; ++c) s_stage[(c * 8 + qq) * SROW + r] = out[c] * sh;
         }
-        named_sync(1, T::PROD);
+        named_sync(1, PROD);
       }
 
-      // ---- A K-step into TMEM (thread-per-row) ----
-      float v[3][8];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int k = k0 + 4 * h;
-        if (k < KV) {
+      // ---- A K-step (this warp's 4 columns, 3 components) into TMEM, thread-per-row ----
+      float v[3][4];
+      {
+        const int k = k0 + 4 * khalf;
+        if (k < 3 * NPK) {
           const int mu = k / NPK, j0 = k - mu * NPK;
           const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
           const int fb = grp == 0 ? 3 : 0;  // E comps read H fields and vice versa
@@ -287,39 +282,39 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             if (grp == 0) {  // (curl H)_x,y,z
-              v[0][4 * h + q] = p1 * zs[q] - p2 * ys[q];
-              v[1][4 * h + q] = p2 * xs[q] - p0 * zs[q];
-              v[2][4 * h + q] = p0 * ys[q] - p1 * xs[q];
+              v[0][q] = p1 * zs[q] - p2 * ys[q];
+              v[1][q] = p2 * xs[q] - p0 * zs[q];
+              v[2][q] = p0 * ys[q] - p1 * xs[q];
             } else {         // -(curl E)_x,y,z
-              v[0][4 * h + q] = p2 * ys[q] - p1 * zs[q];
-              v[1][4 * h + q] = p0 * zs[q] - p2 * xs[q];
-              v[2][4 * h + q] = p1 * xs[q] - p0 * ys[q];
+              v[0][q] = p2 * ys[q] - p1 * zs[q];
+              v[1][q] = p0 * zs[q] - p2 * xs[q];
+              v[2][q] = p1 * xs[q] - p0 * ys[q];
             }
           }
-        } else if (k < KT) {
+        } else if (k >= KV) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) v[c][4 * h + q] = s_stage[((3 * grp + c) * 8 + 4 * h + q) * SROW + row];
+            for (int c = 0; c < 3; ++c) v[c][q] = s_stage[((3 * grp + c) * 8 + 4 * khalf + q) * SROW + row];
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) v[c][4 * h + q] = 0.f;
+            for (int c = 0; c < 3; ++c) v[c][q] = 0.f;
         }
       }
-      float hi[3][8], lo[3][8];
+      float hi[3][4], lo[3][4];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) split_tf32(row_ok ? v[c][q] : 0.f, hi[c][q], lo[c][q]);
+        for (int q = 0; q < 4; ++q) split_tf32(row_ok ? v[c][q] : 0.f, hi[c][q], lo[c][q]);
       mbar_wait(&empty[slot], ((pstep >> 1) & 1) ^ 1);
       fence_after_sync();
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + (3 * grp + c) * 16;
-        tmem_st8(tmem + lane_addr + col, hi[c]);
-        tmem_st8(tmem + lane_addr + col + 8, lo[c]);
+        const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + (3 * grp + c) * 16 + 4 * khalf;
+        tmem_st4(tmem + lane_addr + col, hi[c]);
+        tmem_st4(tmem + lane_addr + col + 8, lo[c]);
       }
       tmem_st_wait();
       fence_before_sync();
@@ -330,13 +325,13 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     // ================= epilogue: accumulators -> LSRK update =================
     mbar_wait(acc_full, it & 1);
     fence_after_sync();
-    named_sync(1, T::PROD);  // staging free (last flux step's reads are done)
-    float* es = s_stage;     // [TE][NPG], one component at a time
+    float* es = s_stage;  // [TE][NPG], one component at a time
     constexpr int RV = NPG / 4;
-    constexpr int PER = (TE * RV + T::PROD - 1) / T::PROD;
+    constexpr int PER = (TE * RV + PROD - 1) / PROD;
+    const int wgrp = warp >> 2;  // 4 groups of 4 quadrant warps
 #pragma unroll 1
     for (int comp = 0; comp < 6; ++comp) {
-      if (grp == (comp & 1)) {  // the group whose quadrant-warps hold this component's rows
+      if (wgrp == (comp & 3)) {  // one quadrant-complete group moves this component to smem
         float* dst = es + row * NPG;
 #pragma unroll
         for (int c0 = 0; c0 < NB; c0 += 8) {
@@ -357,7 +352,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
           }
         }
       }
-      named_sync(1, T::PROD);
+      named_sync(1, PROD);
       const int nvec = nv * RV;
       const int64_t gbase = ((int64_t)comp * a.kf + e0) * NPG;
       const float4* rs = reinterpret_cast<const float4*>(es);
@@ -365,7 +360,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
       if (MODE == MODE_RHS) {
 #pragma unroll
         for (int p = 0; p < PER; ++p) {
-          const int c = tid + p * T::PROD;
+          const int c = tid + p * PROD;
           if (c < nvec) *reinterpret_cast<float4*>(a.out + gbase + (int64_t)c * 4) = rs[c];
         }
       } else {
@@ -373,13 +368,13 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
         if (!a.a_zero) {
 #pragma unroll
           for (int p = 0; p < PER; ++p) {  // all residual loads in flight before any use
-            const int c = tid + p * T::PROD;
+            const int c = tid + p * PROD;
             ro[p] = c < nvec ? __ldcs(reinterpret_cast<const float4*>(a.res + gbase) + c) : make_float4(0, 0, 0, 0);
           }
         }
 #pragma unroll
         for (int p = 0; p < PER; ++p) {
-          const int c = tid + p * T::PROD;
+          const int c = tid + p * PROD;
           if (c < nvec) {
             const float4 rh = rs[c];
             float4 r;
@@ -396,7 +391,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
           }
         }
       }
-      named_sync(1, T::PROD);
+      named_sync(1, PROD);
     }
     fence_before_sync();
   }

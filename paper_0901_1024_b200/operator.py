@@ -47,15 +47,17 @@ def pack_chunks(mat: np.ndarray, chunks: int, vec: int) -> np.ndarray:
 def tc_operand(elem: ReferenceElement, lay) -> np.ndarray:
     """Constant GEMM operand of the tensor-core path, layout of dgm_desc.tc_operand (include/dgm.h).
 
-    B[n][k] = [D_r | D_s | D_t | LIFT][n][k] with each derivative block tc_npk
-    wide; split into a tf32-exact high part (13 low mantissa bits cleared) and
+    B[n][k] = [D_r | D_s | D_t | 0 | LIFT_f0 | .. | LIFT_f3][n][k] with each
+    derivative block tc_npk and each face block tc_nfpk wide; split into a tf32-exact high part (13 low mantissa bits cleared) and
     the float32 remainder, so that hi*x + lo*x carries fp32 accuracy.
     """
-    n_p, nb, npk, steps = elem.num_nodes, lay.tc_nb, lay.tc_npk, lay.tc_steps
+    n_p, n_fp = elem.num_nodes, elem.num_face_nodes
+    nb, npk, steps, kv, nfpk = lay.tc_nb, lay.tc_npk, lay.tc_steps, lay.tc_kv, lay.tc_nfpk
     full = np.zeros((nb, steps * 8))
     for mu in range(3):
         full[:n_p, mu * npk:mu * npk + n_p] = elem.diff[mu]
-    full[:n_p, 3 * npk:3 * npk + elem.lift.shape[1]] = elem.lift
+    for f in range(NUM_FACES):
+        full[:n_p, kv + f * nfpk:kv + f * nfpk + n_fp] = elem.lift[:, f * n_fp:(f + 1) * n_fp]
     hi = (full.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
     lo = (full - hi.astype(np.float64)).astype(np.float32)
     parts = np.stack([hi, lo])                                   # (2, nb, K)

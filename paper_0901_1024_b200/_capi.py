@@ -12,7 +12,7 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdgm.so")
+LIB_PATH = os.environ.get("DGM_LIB") or os.path.join(_HERE, "libdgm.so")
 ABI_VERSION = 2
 GEO_WORDS = 28
 

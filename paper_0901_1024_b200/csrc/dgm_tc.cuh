@@ -34,6 +34,25 @@
 
 namespace dgm {
 
+#ifdef DGM_TC_TRACE
+// Test-only phase timeline of CTA 0 (libdgm_trace.so): (tag, clock64) pairs.
+__device__ long long g_tc_trace[2 * 16384];
+__device__ int g_tc_trace_n;
+__device__ __forceinline__ void tc_trace(int tag) {
+  if (blockIdx.x != 0) return;
+  const int i = atomicAdd(&g_tc_trace_n, 1);
+  if (i < 16384) {
+    g_tc_trace[2 * i] = tag;
+    g_tc_trace[2 * i + 1] = clock64();
+  }
+}
+#define TC_TRACE(tag) tc_trace(tag)
+#else
+#define TC_TRACE(tag) \
+  do {                \
+  } while (0)
+#endif
+
 template <int N>
 struct TcCfg {
   using C = Cfg<N, float>;
@@ -173,6 +192,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
         for (int s = 0; s < KS; ++s, ++mstep) {
           const int slot = mstep & 1;
           mbar_wait(&full[slot], (mstep >> 1) & 1);
+          if (it < 4) TC_TRACE(1000 * it + 500 + 2 * s);  // MMA thread: stage full
           fence_after_sync();
           const uint32_t bh = smem_u32(s_b + s * T::B_STEP_BYTES);
           const uint64_t dbh = desc_kmajor(bh, NB * 16, 128);
@@ -186,6 +206,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
             mma_tf32_ts(acc, ah, dbl, idesc, 1u);
           }
           mma_commit(&empty[slot]);
+          if (it < 4) TC_TRACE(1000 * it + 501 + 2 * s);  // MMA thread: issued
         }
         mma_commit(acc_full);
       }
@@ -194,7 +215,9 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     }
 
     // ================= producers =================
+    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 1);  // tile start
     mbar_wait(load_full, it & 1);
+    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 2);  // rows landed
 
     // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu
     const bool row_ok = row < nv;
@@ -206,6 +229,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
       const int slot = pstep & 1;
       const int k0 = s * 8;
       // ---- surface flux of this step (one face, 8 face nodes): face-node-major mapping ----
+      if (tid == 0 && it < 4) TC_TRACE(1000 * it + 100 + 4 * s);  // step begin
       if (k0 >= KV) {
         named_sync(1, PROD);  // every thread finished reading the staging of the previous step
         const int face = (k0 - KV) / NFPK;
@@ -308,7 +332,9 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int q = 0; q < 4; ++q) split_tf32(row_ok ? v[c][q] : 0.f, hi[c][q], lo[c][q]);
+      if (tid == 0 && it < 4) TC_TRACE(1000 * it + 101 + 4 * s);  // A values ready
       mbar_wait(&empty[slot], ((pstep >> 1) & 1) ^ 1);
+      if (tid == 0 && it < 4) TC_TRACE(1000 * it + 102 + 4 * s);  // stage free
       fence_after_sync();
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -323,7 +349,9 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     }
 
     // ================= epilogue: accumulators -> LSRK update =================
+    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 3);  // all steps produced
     mbar_wait(acc_full, it & 1);
+    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 4);  // accumulators final
     fence_after_sync();
     float* es = s_stage;  // [TE][NPG], one component at a time
     constexpr int RV = NPG / 4;
@@ -393,6 +421,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
       }
       named_sync(1, PROD);
     }
+    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 5);  // epilogue done
     fence_before_sync();
   }
   __syncthreads();

@@ -428,15 +428,11 @@ int dgm_halo_unpack(const dgm_plan* plan, const void* recvbuf, int64_t count, in
 }  // extern "C"
 
 #ifdef DGM_TC_TRACE
-extern "C" int dgm_trace_read(long long* host, int max_pairs) {
+extern "C" int dgm_trace_read(long long* host, int who) {
   int n = 0;
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(&n, dgm::g_tc_trace_n, sizeof(int));
-  if (n > max_pairs) n = max_pairs;
-  if (n > 16384) n = 16384;
-  cudaMemcpyFromSymbol(host, dgm::g_tc_trace, sizeof(long long) * 2 * n);
-  int zero = 0;
-  cudaMemcpyToSymbol(dgm::g_tc_trace_n, &zero, sizeof(int));
+  cudaMemcpyFromSymbol(&n, dgm::g_tc_trace_n, sizeof(int), sizeof(int) * who);
+  cudaMemcpyFromSymbol(host, dgm::g_tc_trace, sizeof(long long) * 2 * n, sizeof(long long) * 2 * 4096 * who);
   return n;
 }
 #endif

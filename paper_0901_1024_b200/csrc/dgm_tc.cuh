@@ -35,21 +35,27 @@
 namespace dgm {
 
 #ifdef DGM_TC_TRACE
-// Test-only phase timeline of CTA 0 (libdgm_trace.so): (tag, clock64) pairs.
-__device__ long long g_tc_trace[2 * 16384];
-__device__ int g_tc_trace_n;
-__device__ __forceinline__ void tc_trace(int tag) {
-  if (blockIdx.x != 0) return;
-  const int i = atomicAdd(&g_tc_trace_n, 1);
-  if (i < 16384) {
-    g_tc_trace[2 * i] = tag;
-    g_tc_trace[2 * i + 1] = clock64();
-  }
-}
-#define TC_TRACE(tag) tc_trace(tag)
+// Test-only phase timeline of CTA 0 (libdgm_trace.so): two tracing threads
+// (producer tid 0, MMA issuer) append (tag, clock64) to their own global slice
+// with plain stores; no atomics on the timed path.
+__device__ long long g_tc_trace[2][2 * 4096];
+__device__ int g_tc_trace_n[2];
+#define TC_TRACE_DECL int tc_tn = 0
+#define TC_TRACE(who, tag)                                     \
+  do {                                                         \
+    if (blockIdx.x == 0 && tc_tn < 4096) {                     \
+      g_tc_trace[who][2 * tc_tn] = (tag);                      \
+      g_tc_trace[who][2 * tc_tn + 1] = clock64();              \
+      ++tc_tn;                                                 \
+      g_tc_trace_n[who] = tc_tn;                               \
+    }                                                          \
+  } while (0)
 #else
-#define TC_TRACE(tag) \
+#define TC_TRACE_DECL \
   do {                \
+  } while (0)
+#define TC_TRACE(who, tag) \
+  do {                     \
   } while (0)
 #endif
 
@@ -158,6 +164,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
   const float inv_m = grp == 0 ? a.inv_eps : a.inv_mu;
   const uint32_t idesc = idesc_tf32(128, NB);
 
+  TC_TRACE_DECL;
   uint32_t pstep = 0;  // producer K-step counter (all tiles)
   uint32_t mstep = 0;  // MMA K-step counter
   int it = 0;
@@ -192,7 +199,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
         for (int s = 0; s < KS; ++s, ++mstep) {
           const int slot = mstep & 1;
           mbar_wait(&full[slot], (mstep >> 1) & 1);
-          if (it < 4) TC_TRACE(1000 * it + 500 + 2 * s);  // MMA thread: stage full
+          if (it < 4) TC_TRACE(1, 1000 * it + 500 + 2 * s);  // MMA thread: stage full
           fence_after_sync();
           const uint32_t bh = smem_u32(s_b + s * T::B_STEP_BYTES);
           const uint64_t dbh = desc_kmajor(bh, NB * 16, 128);
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
             mma_tf32_ts(acc, ah, dbl, idesc, 1u);
           }
           mma_commit(&empty[slot]);
-          if (it < 4) TC_TRACE(1000 * it + 501 + 2 * s);  // MMA thread: issued
+          if (it < 4) TC_TRACE(1, 1000 * it + 501 + 2 * s);  // MMA thread: issued
         }
         mma_commit(acc_full);
       }
@@ -215,9 +222,9 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     }
 
     // ================= producers =================
-    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 1);  // tile start
+    if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 1);  // tile start
     mbar_wait(load_full, it & 1);
-    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 2);  // rows landed
+    if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 2);  // rows landed
 
     // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu
     const bool row_ok = row < nv;
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
       const int slot = pstep & 1;
       const int k0 = s * 8;
       // ---- surface flux of this step (one face, 8 face nodes): face-node-major mapping ----
-      if (tid == 0 && it < 4) TC_TRACE(1000 * it + 100 + 4 * s);  // step begin
+      if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 100 + 4 * s);  // step begin
       if (k0 >= KV) {
         named_sync(1, PROD);  // every thread finished reading the staging of the previous step
         const int face = (k0 - KV) / NFPK;
@@ -332,9 +339,9 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int q = 0; q < 4; ++q) split_tf32(row_ok ? v[c][q] : 0.f, hi[c][q], lo[c][q]);
-      if (tid == 0 && it < 4) TC_TRACE(1000 * it + 101 + 4 * s);  // A values ready
+      if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 101 + 4 * s);  // A values ready
       mbar_wait(&empty[slot], ((pstep >> 1) & 1) ^ 1);
-      if (tid == 0 && it < 4) TC_TRACE(1000 * it + 102 + 4 * s);  // stage free
+      if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 102 + 4 * s);  // stage free
       fence_after_sync();
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -349,9 +356,9 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     }
 
     // ================= epilogue: accumulators -> LSRK update =================
-    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 3);  // all steps produced
+    if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 3);  // all steps produced
     mbar_wait(acc_full, it & 1);
-    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 4);  // accumulators final
+    if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 4);  // accumulators final
     fence_after_sync();
     float* es = s_stage;  // [TE][NPG], one component at a time
     constexpr int RV = NPG / 4;
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
       }
       named_sync(1, PROD);
     }
-    if (tid == 0 && it < 4) TC_TRACE(1000 * it + 5);  // epilogue done
+    if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 5);  // epilogue done
     fence_before_sync();
   }
   __syncthreads();

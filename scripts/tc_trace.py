@@ -20,12 +20,14 @@ op = build_b200_operator(mesh, elem, path="tensor")
 u = op.to_padded(CavityMode(1, 1, 1, (1.0, 1.0, 1.0)).evaluate(map_nodes(mesh, elem), 0.0))
 lib = _capi.load()
 lib.dgm_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
-buf = np.zeros(2 * 16384, dtype=np.int64)
 op.advance(u, 1e-4, 1, use_graph=False)
-lib.dgm_trace_read(buf.ctypes.data, 16384)  # reset after warm-up
 op.lsrk_stage(u, op._buffers().alt, op._buffers().res, -0.4, 0.3, 1e-4)
-n = lib.dgm_trace_read(buf.ctypes.data, 16384)
-ev = buf[: 2 * n].reshape(-1, 2)
+evs = []
+for who in (0, 1):
+    buf = np.zeros(2 * 4096, dtype=np.int64)
+    n = lib.dgm_trace_read(buf.ctypes.data, who)
+    evs.append(buf[: 2 * n].reshape(-1, 2))
+ev = np.concatenate(evs)
 ev = ev[np.argsort(ev[:, 1], kind="stable")]
 t0 = ev[0, 1]
 for tag, t in ev:

@@ -149,7 +149,54 @@ __global__ void __launch_bounds__(128) probe_ts_kernel(const float* __restrict__
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// Throughput microbenchmark: one thread issues `reps` kind::tf32 MMAs (M=128, N=n,
+// K=8) back to back into one accumulator, A from smem (ts=0) or TMEM (ts=1).
+__global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts, long long* cycles) {
+  using namespace dgm::tc;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  float* a_s = reinterpret_cast<float*>(smem);       // 128 x 8
+  float* b_s = a_s + 128 * 8;                          // n x 8
+  for (int i = threadIdx.x; i < (128 + n) * 8; i += blockDim.x) a_s[i] = 0.f;
+  if (threadIdx.x < 32) tmem_alloc(&tmem_base, 512);
+  if (threadIdx.x == 32) {
+    mbar_init(&mbar, 1);
+    mbar_init_fence();
+  }
+  fence_async_smem();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_tf32(128, n);
+    const uint64_t ad = desc_kmajor(smem_u32(a_s), 128 * 16, 128);
+    const uint64_t bd = desc_kmajor(smem_u32(b_s), n * 16, 128);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      if (ts) mma_tf32_ts(tmem, tmem + 256, bd, idesc, r > 0);
+      else mma_tf32(tmem, ad, bd, idesc, r > 0);
+    }
+    const long long t1 = clock64();
+    mma_commit(&mbar);
+    mbar_wait(&mbar, 0);
+    const long long t2 = clock64();
+    cycles[0] = t1 - t0;
+    cycles[1] = t2 - t0;
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
 }  // namespace
+
+extern "C" int dgm_probe_mma_rate(int n, int reps, int ts, long long* cycles_dev) {
+  const size_t smem = (size_t)(128 + n) * 8 * 4;
+  probe_rate_kernel<<<1, 128, smem>>>(n, reps, ts, cycles_dev);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
 
 extern "C" int dgm_probe_tf32_gemm_ts(const float* a, const float* b, float* c, int n, int k, int passes,
                                       void* stream) {

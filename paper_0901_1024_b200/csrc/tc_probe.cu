@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(128) probe_ts_kernel(const float* __restrict__
 
 // Throughput microbenchmark: one thread issues `reps` kind::tf32 MMAs (M=128, N=n,
 // K=8) back to back into one accumulator, A from smem (ts=0) or TMEM (ts=1).
-__global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts, long long* cycles) {
+__global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts, int nacc, long long* cycles) {
   using namespace dgm::tc;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -175,8 +175,9 @@ __global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts
     const uint64_t bd = desc_kmajor(smem_u32(b_s), n * 16, 128);
     const long long t0 = clock64();
     for (int r = 0; r < reps; ++r) {
-      if (ts) mma_tf32_ts(tmem, tmem + 256, bd, idesc, r > 0);
-      else mma_tf32(tmem, ad, bd, idesc, r > 0);
+      const uint32_t acc = tmem + (uint32_t)((r % nacc) * n);
+      if (ts) mma_tf32_ts(acc, tmem + 448, bd, idesc, r >= nacc);
+      else mma_tf32(acc, ad, bd, idesc, r >= nacc);
     }
     const long long t1 = clock64();
     mma_commit(&mbar);
@@ -192,9 +193,10 @@ __global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts
 
 }  // namespace
 
-extern "C" int dgm_probe_mma_rate(int n, int reps, int ts, long long* cycles_dev) {
+extern "C" int dgm_probe_mma_rate(int n, int reps, int ts, int nacc, long long* cycles_dev) {
+  if (nacc < 1 || nacc * n > 448) return -1;
   const size_t smem = (size_t)(128 + n) * 8 * 4;
-  probe_rate_kernel<<<1, 128, smem>>>(n, reps, ts, cycles_dev);
+  probe_rate_kernel<<<1, 128, smem>>>(n, reps, ts, nacc, cycles_dev);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

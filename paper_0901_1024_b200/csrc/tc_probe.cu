@@ -169,22 +169,42 @@ __global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tmem_base;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // whole warp runs the (uniform) issue loop, one elected lane issues
     const uint32_t idesc = idesc_tf32(128, n);
     const uint64_t ad = desc_kmajor(smem_u32(a_s), 128 * 16, 128);
     const uint64_t bd = desc_kmajor(smem_u32(b_s), n * 16, 128);
+    __syncwarp();
     const long long t0 = clock64();
-    for (int r = 0; r < reps; ++r) {
-      const uint32_t acc = tmem + (uint32_t)((r % nacc) * n);
-      if (ts) mma_tf32_ts(acc, tmem + 448, bd, idesc, r >= nacc);
-      else mma_tf32(acc, ad, bd, idesc, r >= nacc);
+    if (nacc == 1) {
+      for (int r = 0; r < reps; ++r) {
+        if (elect_one()) {
+          if (ts) mma_tf32_ts(tmem, tmem + 448, bd, idesc, r > 0);
+          else mma_tf32(tmem, ad, bd, idesc, r > 0);
+        }
+        __syncwarp();
+      }
+    } else {
+      for (int r = 0; r < reps; r += 6) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          if (elect_one()) {
+            const uint32_t acc = tmem + (uint32_t)(c * 64);
+            if (ts) mma_tf32_ts(acc, tmem + 448, bd, idesc, r > 0);
+            else mma_tf32(acc, ad, bd, idesc, r > 0);
+          }
+          __syncwarp();
+        }
+      }
     }
     const long long t1 = clock64();
-    mma_commit(&mbar);
+    if (elect_one()) mma_commit(&mbar);
+    __syncwarp();
     mbar_wait(&mbar, 0);
     const long long t2 = clock64();
-    cycles[0] = t1 - t0;
-    cycles[1] = t2 - t0;
+    if (threadIdx.x == 0) {
+      cycles[0] = t1 - t0;
+      cycles[1] = t2 - t0;
+    }
   }
   fence_before_sync();
   __syncthreads();
@@ -194,7 +214,7 @@ __global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts
 }  // namespace
 
 extern "C" int dgm_probe_mma_rate(int n, int reps, int ts, int nacc, long long* cycles_dev) {
-  if (nacc < 1 || nacc * n > 448) return -1;
+  if (nacc < 1 || (nacc > 1 && n > 64) || n > 256) return -1;
   const size_t smem = (size_t)(128 + n) * 8 * 4;
   probe_rate_kernel<<<1, 128, smem>>>(n, reps, ts, nacc, cycles_dev);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;

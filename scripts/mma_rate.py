@@ -9,9 +9,9 @@ lib = ctypes.CDLL(os.path.join(ROOT, "paper_0901_1024_b200", "libdgm_probe.so"))
 lib.dgm_probe_mma_rate.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p]
 out = torch.zeros(2, dtype=torch.int64, device="cuda")
 for ts in (0, 1):
-    for n in (16, 48, 64, 96, 128, 224):
-        for nacc in (1, 2, 3, 6):
-            if nacc * n > 448:
+    for n in (16, 48, 64, 128, 256):
+        for nacc in (1, 6):
+            if nacc > 1 and n > 64:
                 continue
             reps = 1008
             assert lib.dgm_probe_mma_rate(n, reps, ts, nacc, out.data_ptr()) == 0

@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts
     if (nacc == 1) {
       for (int r = 0; r < reps; ++r) {
         if (elect_one()) {
-          if (ts) mma_tf32_ts(tmem, tmem + 448, bd, idesc, r > 0);
+          if (ts == 2) mma_bf16(tmem, ad, bd, idesc_bf16(128, n), r > 0);
+          else if (ts) mma_tf32_ts(tmem, tmem + 448, bd, idesc, r > 0);
           else mma_tf32(tmem, ad, bd, idesc, r > 0);
         }
         __syncwarp();

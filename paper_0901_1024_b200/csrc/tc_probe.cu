@@ -175,7 +175,24 @@ __global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts
     const uint64_t bd = desc_kmajor(smem_u32(b_s), n * 16, 128);
     __syncwarp();
     const long long t0 = clock64();
-    if (nacc == 1) {
+    if (nacc == 0) {  // unrolled bursts of 48 MMAs, loop-invariant operands, one elect per burst
+      const uint32_t idb = idesc_bf16(128, n);
+      for (int r = 0; r < reps; r += 48) {
+        if (elect_one()) {
+          if (ts == 2) {
+#pragma unroll
+            for (int q = 0; q < 48; ++q) mma_bf16(tmem + (q % 6) * 64, ad, bd, idb, 1u);
+          } else if (ts == 1) {
+#pragma unroll
+            for (int q = 0; q < 48; ++q) mma_tf32_ts(tmem + (q % 6) * 64, tmem + 448, bd, idesc, 1u);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 48; ++q) mma_tf32(tmem + (q % 6) * 64, ad, bd, idesc, 1u);
+          }
+        }
+        __syncwarp();
+      }
+    } else if (nacc == 1) {
       for (int r = 0; r < reps; ++r) {
         if (elect_one()) {
           if (ts == 2) mma_bf16(tmem, ad, bd, idesc_bf16(128, n), r > 0);
@@ -215,7 +232,7 @@ __global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts
 }  // namespace
 
 extern "C" int dgm_probe_mma_rate(int n, int reps, int ts, int nacc, long long* cycles_dev) {
-  if (nacc < 1 || (nacc > 1 && n > 64) || n > 256) return -1;
+  if (nacc < 0 || (nacc != 1 && n > 64) || n > 256) return -1;
   const size_t smem = (size_t)(128 + n) * 8 * 4;
   probe_rate_kernel<<<1, 128, smem>>>(n, reps, ts, nacc, cycles_dev);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;

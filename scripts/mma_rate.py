@@ -10,10 +10,10 @@ lib.dgm_probe_mma_rate.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p]
 out = torch.zeros(2, dtype=torch.int64, device="cuda")
 for ts in (0, 1, 2):
     for n in (16, 48, 64, 128, 256):
-        for nacc in (1, 6):
-            if (nacc > 1 and n > 64) or (ts == 2 and nacc > 1):
+        for nacc in (0, 1, 6):
+            if (nacc != 1 and n > 64) or (ts == 2 and nacc == 6):
                 continue
-            reps = 1008
+            reps = 1008 if nacc else 1008 // 48 * 48
             assert lib.dgm_probe_mma_rate(n, reps, ts, nacc, out.data_ptr()) == 0
             torch.cuda.synchronize()
             issue, done = out.tolist()

@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
   uint64_t* load_full = bar + 4; // tile rows landed
   uint64_t* acc_full = bar + 5;  // accumulators final
   uint64_t* b_full = bar + 6;    // resident B operand landed
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 7);
+  uint64_t* tile_free = bar + 7; // producers finished reading this tile's smem rows
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 8);
   uint8_t* s_fmask = smem + T::OFF_FMASK;
   uint8_t* s_ptab = smem + T::OFF_PTAB;
 
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     mbar_init(load_full, 1);
     mbar_init(acc_full, 1);
     mbar_init(b_full, 1);
+    mbar_init(tile_free, T::PWARPS);
     mbar_init_fence();
   }
   for (int c = tid; c < 4 * NFP; c += blockDim.x) s_fmask[c] = a.fmask[c];
@@ -166,15 +168,15 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
 
   TC_TRACE_DECL;
   uint32_t pstep = 0;  // producer K-step counter (all tiles)
-  uint32_t mstep = 0;  // MMA K-step counter
   int it = 0;
-  for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
-    const int64_t e0 = a.e_begin + (int64_t)tile * TE;
-    const int nv = (int)min((int64_t)TE, a.e_end - e0);
-    __syncthreads();  // previous tile's epilogue is done with s_u / s_stage / s_geo
-
-    if (warp == T::PWARPS) {
-      if (lane == 0) {
+  if (warp == T::PWARPS) {
+    // ================= control warp: tile loads + MMA issue (warp-uniform) =================
+    uint32_t mstep = 0;
+    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+      const int64_t e0 = a.e_begin + (int64_t)tile * TE;
+      const int nv = (int)min((int64_t)TE, a.e_end - e0);
+      if (it > 0) mbar_wait(tile_free, (it - 1) & 1);  // previous tile's rows consumed
+      if (elect_one()) {
         const uint32_t rowbytes = (uint32_t)nv * NPG * 4;
         const uint32_t geobytes = (uint32_t)nv * GEO_WORDS * 4, conbytes = (uint32_t)nv * 16;
         mbar_expect_tx(load_full, 6 * rowbytes + geobytes + 2 * conbytes);
@@ -194,32 +196,39 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
           prefetch_l2(a.nbr + n0 * 4, nn * 16);
           prefetch_l2(a.code + n0 * 4, nn * 16);
         }
-        if (it == 0) mbar_wait(b_full, 0);
-        // ---------------- MMA issuer ----------------
-        for (int s = 0; s < KS; ++s, ++mstep) {
-          const int slot = mstep & 1;
-          mbar_wait(&full[slot], (mstep >> 1) & 1);
-          if (it < 4) TC_TRACE(1, 1000 * it + 500 + 2 * s);  // MMA thread: stage full
-          fence_after_sync();
+      }
+      __syncwarp();
+      if (it == 0) mbar_wait(b_full, 0);
+      for (int s = 0; s < KS; ++s, ++mstep) {
+        const int slot = mstep & 1;
+        mbar_wait(&full[slot], (mstep >> 1) & 1);
+        if (it < 4) TC_TRACE(1, 1000 * it + 500 + 2 * s);  // stage full
+        fence_after_sync();
+        if (elect_one()) {
           const uint32_t bh = smem_u32(s_b + s * T::B_STEP_BYTES);
           const uint64_t dbh = desc_kmajor(bh, NB * 16, 128);
           const uint64_t dbl = desc_kmajor(bh + 2 * NB * 16, NB * 16, 128);
+          const uint32_t abase = tmem + T::A_COL0 + slot * T::A_STAGE_COLS;
+          const uint32_t acc0 = s > 0 ? 1u : 0u;
+          // pass-major order: consecutive MMAs hit different accumulators
 #pragma unroll
-          for (int c = 0; c < 6; ++c) {
-            const uint32_t acc = tmem + c * NB;
-            const uint32_t ah = tmem + T::A_COL0 + slot * T::A_STAGE_COLS + c * 16;
-            mma_tf32_ts(acc, ah, dbh, idesc, s > 0 ? 1u : 0u);
-            mma_tf32_ts(acc, ah + 8, dbh, idesc, 1u);
-            mma_tf32_ts(acc, ah, dbl, idesc, 1u);
-          }
+          for (int c = 0; c < 6; ++c) mma_tf32_ts(tmem + c * NB, abase + c * 16, dbh, idesc, acc0);
+#pragma unroll
+          for (int c = 0; c < 6; ++c) mma_tf32_ts(tmem + c * NB, abase + c * 16 + 8, dbh, idesc, 1u);
+#pragma unroll
+          for (int c = 0; c < 6; ++c) mma_tf32_ts(tmem + c * NB, abase + c * 16, dbl, idesc, 1u);
           mma_commit(&empty[slot]);
-          if (it < 4) TC_TRACE(1, 1000 * it + 501 + 2 * s);  // MMA thread: issued
         }
-        mma_commit(acc_full);
+        __syncwarp();
+        if (it < 4) TC_TRACE(1, 1000 * it + 501 + 2 * s);  // issued
       }
+      if (elect_one()) mma_commit(acc_full);
       __syncwarp();
-      continue;
     }
+  } else {
+  for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
+    const int64_t e0 = a.e_begin + (int64_t)tile * TE;
+    const int nv = (int)min((int64_t)TE, a.e_end - e0);
 
     // ================= producers =================
     if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 1);  // tile start
@@ -357,6 +366,8 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
 
     // ================= epilogue: accumulators -> LSRK update =================
     if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 3);  // all steps produced
+    __syncwarp();
+    if (lane == 0) mbar_arrive(tile_free);  // smem tile rows may be refilled with the next tile
     mbar_wait(acc_full, it & 1);
     if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 4);  // accumulators final
     fence_after_sync();
@@ -391,7 +402,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
       const int nvec = nv * RV;
       const int64_t gbase = ((int64_t)comp * a.kf + e0) * NPG;
       const float4* rs = reinterpret_cast<const float4*>(es);
-      const float4* us = reinterpret_cast<const float4*>(s_u + comp * TE * NPG);
+      const float4* ug = reinterpret_cast<const float4*>(a.u + gbase);  // L2-hot, smem is being refilled
       if (MODE == MODE_RHS) {
 #pragma unroll
         for (int p = 0; p < PER; ++p) {
@@ -399,13 +410,14 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
           if (c < nvec) *reinterpret_cast<float4*>(a.out + gbase + (int64_t)c * 4) = rs[c];
         }
       } else {
-        float4 ro[PER];
-        if (!a.a_zero) {
+        float4 ro[PER], uo[PER];
 #pragma unroll
-          for (int p = 0; p < PER; ++p) {  // all residual loads in flight before any use
-            const int c = tid + p * PROD;
-            ro[p] = c < nvec ? __ldcs(reinterpret_cast<const float4*>(a.res + gbase) + c) : make_float4(0, 0, 0, 0);
-          }
+        for (int p = 0; p < PER; ++p) {  // all loads in flight before any use
+          const int c = tid + p * PROD;
+          const bool ok = c < nvec;
+          uo[p] = ok ? __ldg(ug + c) : make_float4(0, 0, 0, 0);
+          ro[p] = (ok && !a.a_zero) ? __ldcs(reinterpret_cast<const float4*>(a.res + gbase) + c)
+                                    : make_float4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int p = 0; p < PER; ++p) {
@@ -420,9 +432,8 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
                               a.a * ro[p].z + a.dt * rh.z, a.a * ro[p].w + a.dt * rh.w);
             }
             __stcs(reinterpret_cast<float4*>(a.res + gbase) + c, r);
-            const float4 uo = us[c];
             __stcs(reinterpret_cast<float4*>(a.u_out + gbase) + c,
-                   make_float4(uo.x + a.b * r.x, uo.y + a.b * r.y, uo.z + a.b * r.z, uo.w + a.b * r.w));
+                   make_float4(uo[p].x + a.b * r.x, uo[p].y + a.b * r.y, uo[p].z + a.b * r.z, uo[p].w + a.b * r.w));
           }
         }
       }
@@ -430,6 +441,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     }
     if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 5);  // epilogue done
     fence_before_sync();
+  }
   }
   __syncthreads();
   fence_after_sync();

@@ -8,3 +8,4 @@ timeout 600 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; e
 timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_tc.json 2> gpurun_out/bench_tc.err
 timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --path simt > gpurun_out/bench_simt.json 2> gpurun_out/bench_simt.err
 echo done
+timeout 300 python scripts/tc_trace.py 30 30 30 > gpurun_out/tc_trace.txt 2>&1

@@ -91,7 +91,7 @@ struct TcCfg {
                                             : (size_t)TE * NPG * 4;
   static constexpr size_t OFF_STAGE = OFF_B + (size_t)KS * B_STEP_BYTES;
   static constexpr size_t OFF_BAR = OFF_STAGE + STAGE_BYTES;
-  static constexpr size_t OFF_FMASK = OFF_BAR + 64;
+  static constexpr size_t OFF_FMASK = OFF_BAR + 128;  // 9 mbarriers + TMEM base address
   static constexpr size_t OFF_PTAB = OFF_FMASK + (4 * NFP + 15) / 16 * 16;
   static constexpr size_t SMEM_FIXED = OFF_PTAB;   // + ncodes * NFP
   static constexpr size_t B_FLOATS = (size_t)KS * 2 * 2 * NB * 4;  // packed operand in global

@@ -428,6 +428,9 @@ int dgm_halo_unpack(const dgm_plan* plan, const void* recvbuf, int64_t count, in
 }  // extern "C"
 
 #ifdef DGM_TC_TRACE
+extern "C" int dgm_hang_read(unsigned int* host) {
+  return (int)cudaMemcpyFromSymbol(host, dgm::tc::g_hang, sizeof(unsigned int) * 8);
+}
 extern "C" int dgm_trace_read(long long* host, int who) {
   int n = 0;
   cudaDeviceSynchronize();

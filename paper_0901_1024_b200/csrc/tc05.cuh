@@ -102,6 +102,35 @@ __device__ __forceinline__ void mbar_arrive(void* mbar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
 }
 
+#ifdef DGM_TC_TRACE
+__device__ unsigned int g_hang[8];
+__device__ __forceinline__ bool mbar_try(void* mbar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(mbar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Trace build: a wait that never completes records who/what and traps.
+__device__ __noinline__ void mbar_wait(void* mbar, uint32_t parity) {
+  for (uint32_t i = 0; !mbar_try(mbar, parity); ++i) {
+    if (i == (1u << 22)) {
+      if (atomicCAS(&g_hang[0], 0u, 1u) == 0u) {
+        g_hang[1] = blockIdx.x;
+        g_hang[2] = threadIdx.x;
+        g_hang[3] = smem_u32(mbar);
+        g_hang[4] = parity;
+        __threadfence_system();
+      }
+      __trap();
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(void* mbar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -113,6 +142,7 @@ __device__ __forceinline__ void mbar_wait(void* mbar, uint32_t parity) {
       "r"(parity), "r"(0x989680u)
       : "memory");
 }
+#endif
 
 // Generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operands).
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

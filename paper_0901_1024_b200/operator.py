@@ -367,10 +367,17 @@ class B200MaxwellOperator:
         return self.advance(u, dt, 1, use_graph=False)
 
     # ---------------------------------------------------------- diagnostics
-    def mass_norm(self, u: torch.Tensor, w_e: float = 1.0, w_h: float = 1.0) -> torch.Tensor:
-        """Device scalar sum_k J_k sum_f w_f u^T M u (float64 tensor, no sync)."""
+    def mass_norm(self, u: torch.Tensor, w_e: float = 1.0, w_h: float = 1.0,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+        """Device scalar sum_k J_k sum_f w_f u^T M u (float64 tensor, no sync).
+
+        With ``out`` (a zeroed float64 device slot) the value is accumulated there.
+        """
         self._check_padded(u)
-        out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        if out is None:
+            out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        elif out.dtype != torch.float64 or out.device != self.device or out.numel() < 1:
+            raise ValueError("out must be a float64 device tensor on the operator's device")
         _capi.check(self._lib.dgm_mass_norm(self._plan, u.data_ptr(), self._mass.data_ptr(), self._det.data_ptr(),
                                             float(w_e), float(w_h), out.data_ptr(), 0, self.num_elements,
                                             self._stream()), "dgm_mass_norm")

@@ -194,6 +194,8 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
       }
       using TC = dgm::TcCfg<N>;
       tc_smem = (TC::SMEM_FIXED + (size_t)d.num_codes * TC::NFP + 127) & ~size_t(127);
+      // one CTA per SM: the kernel allocates all 512 TMEM columns
+      if (tc_smem < 120 * 1024) tc_smem = 120 * 1024;
       if (tc_smem > 227 * 1024) {
         if (d.path == DGM_PATH_TENSOR) return fail(DGM_ERR_UNSUPPORTED, "tensor path smem %zu too large", tc_smem);
         return DGM_OK;

@@ -194,8 +194,8 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
       }
       using TC = dgm::TcCfg<N>;
       tc_smem = (TC::SMEM_FIXED + (size_t)d.num_codes * TC::NFP + 127) & ~size_t(127);
-      // one CTA per SM: the kernel allocates all 512 TMEM columns
-      if (tc_smem < 120 * 1024) tc_smem = 120 * 1024;
+      // at most two CTAs per SM: each allocates 256 of the 512 TMEM columns
+      if (tc_smem < 80 * 1024) tc_smem = 80 * 1024;
       if (tc_smem > 227 * 1024) {
         if (d.path == DGM_PATH_TENSOR) return fail(DGM_ERR_UNSUPPORTED, "tensor path smem %zu too large", tc_smem);
         return DGM_OK;
@@ -301,8 +301,8 @@ int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, vo
         targs.bpack = static_cast<const float*>(d.tc_operand);
         const int64_t tt = (e_end - e_begin + TC::TE - 1) / TC::TE;
         targs.num_tiles = (int)tt;
-        const int grid = (int)(tt < plan->num_sms ? tt : plan->num_sms);
-        dgm::tc_stage_kernel<N, MODE><<<grid, TC::THREADS, plan->tc_smem, static_cast<cudaStream_t>(stream)>>>(targs);
+        dgm::tc_stage_kernel<N, MODE><<<(unsigned)tt, TC::THREADS, plan->tc_smem, static_cast<cudaStream_t>(stream)>>>(
+            targs);
         return cuda_check(cudaGetLastError(), "tc_stage_kernel launch");
       }
     }

@@ -8,34 +8,36 @@
 //   f^(c)    = upwind_bracket_c * face_jacobian / det_J / (eps|mu)
 //
 // because d/dx_nu u = sum_mu rx[mu][nu] D_mu u and rx is constant per element.
-// So with A[e][k] = [w_0 | w_1 | w_2 | pad | f_face0 | .. | f_face3] and the
+// So with A[row][k] = [w_0 | w_1 | w_2 | pad | f_face0 | .. | f_face3] and the
 // constant B[n][k] = [D_0 | D_1 | D_2 | 0 | LIFT_face0 | .. ] (rows n = output
 // node; every face block padded to NFPK = ceil8(Nfp) so a flux K-step never
-// straddles two faces), one tcgen05.mma chain per component computes the full
-// RHS of 128 elements (M = 128 TMEM lanes, one element per lane).  fp32
+// straddles two faces), tcgen05.mma chains compute the full RHS.  fp32
 // accuracy comes from 3xTF32 (A_hi B_hi + A_lo B_hi + A_hi B_lo), exact splits.
 //
-// Roles (544 threads, one CTA per SM, persistent over 128-element tiles):
-//   warps 0-15 producers.
-//     A K-step: thread-per-row (row = TMEM lane); warp w serves lane quadrant
-//     w%4, component group (w/8: E components from H fields, or H components
-//     from E fields) and K half ((w/4)%2); tcgen05.st of hi and lo parts into
-//     a 2-stage A ring in TMEM.
-//     Surface flux: once per face (all NFPK node slots, 2 K-steps at N=3,4),
-//     node-major mapping (NFPK lanes per element row, coalesced neighbour
-//     gathers, all loads in flight before any use) into smem staging.
-//     Epilogue: per component, one quadrant-complete warp group moves the
-//     accumulator TMEM -> smem (double-buffered) while all producers apply the
-//     LSRK update of the previous component with coalesced 16-B accesses; u
-//     comes from the tile's smem rows, res was L2-prefetched at tile start.
-//     After component c the smem slab of field c is released to the loader.
-//   warp 16 (control, warp-uniform; one elected lane issues):
-//     cp.async.bulk of each tile's geometry / connectivity rows (as soon as
-//     the producers finish the K-loop) and field slabs (as soon as the
-//     epilogue releases them), L2 prefetch of the residual, of the next tile
-//     and of every out-of-tile face neighbour's rows, the B operand ring (two
-//     K-steps ahead), and the 18 MMAs of each K-step as one burst.
-// TMEM: [0, 6*NB) accumulators; two A stages of 6 x (8 hi + 8 lo) columns.
+// Tiling: a CTA owns TE = 64 consecutive elements.  The 6 x 64 GEMM rows are
+// three M = 128 tiles; M-tile t holds component t (E_t) of the 64 elements in
+// TMEM lanes 0-63 and component t+3 (H_t) in lanes 64-127, so every MMA is a
+// full 128-lane instruction and a CTA needs only 3*NB accumulator columns plus
+// a 2-stage A ring (<= 256 TMEM columns) and ~103 KB of shared memory at N=4:
+// two CTAs share an SM and hide each other's gather / barrier latencies.
+//
+// Roles (320 threads):
+//   warps 0-7 producers, thread-per-TMEM-lane: warp w serves lane quadrant
+//     q = w%4 (lanes 32q..32q+31: element (q%2)*32 + lane, E components for
+//     q < 2, H components for q >= 2) and K half w/4.
+//     A K-step: 4 columns x 3 M-tiles, tcgen05.st of the tf32 hi and lo parts.
+//     Surface flux: once per face (all NFPK node slots), node-major mapping
+//     (coalesced neighbour gathers, all loads in flight before any use) into
+//     smem staging that the face K-steps read.
+//     Epilogue per M-tile: quadrant warps move the accumulator TMEM -> smem,
+//     then all producers apply the LSRK update with coalesced 16-B accesses
+//     (u from the tile's smem rows, res L2-prefetched at CTA start).
+//   warp 8 (MMA, warp-uniform; one elected lane issues): the 9 MMAs of each
+//     K-step as one burst, committed to the A stage's `empty` barrier.
+//   warp 9 (loader): cp.async.bulk of the tile's rows (one mbarrier with a tx
+//     count), L2 prefetch of the residual, and the B operand ring (BAHEAD
+//     K-steps ahead, a slot refilled once the MMAs that read it completed) --
+//     kept off the MMA warp because bulk-copy issue can stall on the TMA queue.
 #pragma once
 
 #include "dgm_stage.cuh"
@@ -78,19 +80,21 @@ struct TcCfg {
   static constexpr int KV = (3 * NPK + 7) / 8 * 8; // volume part of K, padded to a K step
   static constexpr int KT = KV + 4 * NFPK;
   static constexpr int KS = KT / 8;                // K steps (one kind::tf32 MMA each)
-  static constexpr int TE = 128;
-  static constexpr int PWARPS = 16;
+  static constexpr int TE = 64;                    // elements per CTA
+  static constexpr int MT = 3;                     // M-tiles (E_t | H_t)
+  static constexpr int PWARPS = 8;
   static constexpr int PROD = 32 * PWARPS;         // producer threads
-  static constexpr int THREADS = PROD + 32;
-  static constexpr int ACC_COLS = 6 * NB;
+  static constexpr int THREADS = PROD + 64;        // + MMA warp + loader warp
+  static constexpr int ACC_COLS = MT * NB;
   static constexpr int A_COL0 = (ACC_COLS + 31) / 32 * 32;
-  static constexpr int A_STAGE_COLS = 6 * 16;      // 6 components x (8 hi + 8 lo)
-  static constexpr int TMEM_COLS = 512;
-  static_assert(A_COL0 + 2 * A_STAGE_COLS <= TMEM_COLS, "TMEM budget");
+  static constexpr int A_STAGE_COLS = MT * 16;     // 3 M-tiles x (8 hi + 8 lo)
+  static constexpr int TMEM_COLS = 256;
+  static_assert(A_COL0 + 2 * A_STAGE_COLS <= TMEM_COLS, "TMEM budget (two CTAs per SM)");
   static constexpr int SROW = TE + 4;              // flux staging row stride
   static constexpr int B_STEP_BYTES = 2 * 2 * NB * 16;   // hi/lo x 2 chunks x NB rows x 16 B
-  static constexpr int NBS = 4;                    // B ring slots (two K-steps ahead of the MMAs)
-  static constexpr uint32_t ROWS_BYTES = TE * NPG * 4;   // one field slab of one tile
+  static constexpr int NBS = 6;                    // B ring slots
+  static constexpr int BAHEAD = NBS - 2;           // B loaded this many K-steps ahead of its MMAs
+  static constexpr uint32_t ROWS_BYTES = TE * NPG * 4;   // one field slab of the tile
   static constexpr int ITEMS = TE * NFPK / PROD;   // (row, face node) flux items per thread
   static_assert(ITEMS * PROD == TE * NFPK, "flux items must tile the producers");
   // shared-memory carve-up (bytes)
@@ -103,7 +107,7 @@ struct TcCfg {
   static constexpr size_t EPI_BYTES = (size_t)2 * ROWS_BYTES;
   static constexpr size_t OFF_STAGE = OFF_B + (size_t)NBS * B_STEP_BYTES;
   static constexpr size_t OFF_BAR = OFF_STAGE + (FLUX_BYTES > EPI_BYTES ? FLUX_BYTES : EPI_BYTES);
-  static constexpr size_t OFF_FMASK = OFF_BAR + 256;  // 17 mbarriers + TMEM base address
+  static constexpr size_t OFF_FMASK = OFF_BAR + 128;  // 10 mbarriers + TMEM base address
   static constexpr size_t OFF_PTAB = OFF_FMASK + (4 * NFP + 15) / 16 * 16;
   static constexpr size_t SMEM_FIXED = OFF_PTAB;   // + ncodes * NFP
   static constexpr size_t B_FLOATS = (size_t)KS * 2 * 2 * NB * 4;  // packed operand in global
@@ -116,12 +120,12 @@ struct TcArgs {
 };
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const TcArgs args) {
+__global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const TcArgs args) {
   using T = TcCfg<N>;
   using namespace tc;
   constexpr int TE = T::TE, NPG = T::NPG, NP = T::NP, NFP = T::NFP, NB = T::NB, NFPK = T::NFPK;
   constexpr int KS = T::KS, KV = T::KV, NPK = T::NPK, SROW = T::SROW, PROD = T::PROD, NBS = T::NBS;
-  constexpr int ITEMS = T::ITEMS;
+  constexpr int ITEMS = T::ITEMS, MT = T::MT;
   const StageArgs<float>& a = args.s;
 
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -130,21 +134,26 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
   int* s_nbr = reinterpret_cast<int*>(smem + T::OFF_NBR);
   int* s_code = reinterpret_cast<int*>(smem + T::OFF_CODE);
   unsigned char* s_b = smem + T::OFF_B;
-  float* s_stage = reinterpret_cast<float*>(smem + T::OFF_STAGE);  // flux of one face | 2 epilogue rows buffers
+  float* s_stage = reinterpret_cast<float*>(smem + T::OFF_STAGE);  // flux of one face | epilogue rows
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
   uint64_t* full = bar + 0;        // [2] producers -> MMA (A stage written)
   uint64_t* empty = bar + 2;       // [2] MMA commit -> A stage / B slot reusable
   uint64_t* load_full = bar + 4;   // tile rows landed
   uint64_t* acc_full = bar + 5;    // accumulators final
-  uint64_t* tile_free = bar + 6;   // producers finished the K-loop (geometry / connectivity reusable)
-  uint64_t* slab_free = bar + 7;   // [6] epilogue finished reading field slab c
-  uint64_t* b_full = bar + 13;     // [NBS] B ring slot landed
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 17);
+  uint64_t* b_full = bar + 6;      // [NBS] B ring slot landed
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 6 + NBS);
+  static_assert((6 + NBS) * 8 + 4 <= 128, "barrier region");
   uint8_t* s_fmask = smem + T::OFF_FMASK;
   uint8_t* s_ptab = smem + T::OFF_PTAB;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t fstride = a.kf * NPG;
+  const int64_t e0 = a.e_begin + (int64_t)blockIdx.x * TE;
+  const int nv = (int)min((int64_t)TE, a.e_end - e0);
+  // Each CTA walks the K-steps in a rotated order (a sum; any order is exact up to rounding) starting
+  // at a volume step, so co-running CTAs fetch different slices of the shared B operand from L2
+  // instead of all hitting the same lines at once.  Face steps stay contiguous.
+  const int rot = (int)(blockIdx.x % (unsigned)(KV / 8));
 
   if (warp == 0) tmem_alloc(s_tmem, T::TMEM_COLS);
   if (tid == PROD) {
@@ -154,8 +163,6 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
     mbar_init(&empty[1], 1);
     mbar_init(load_full, 1);
     mbar_init(acc_full, 1);
-    mbar_init(tile_free, T::PWARPS);
-    for (int c = 0; c < 6; ++c) mbar_init(&slab_free[c], 1);
     for (int i = 0; i < NBS; ++i) mbar_init(&b_full[i], 1);
     mbar_init_fence();
   }
@@ -167,271 +174,246 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
   const uint32_t tmem = *s_tmem;
   TC_TRACE_DECL;
 
-  if (warp == T::PWARPS) {
-    // ================= control warp =================
-    const uint32_t idesc = idesc_tf32(128, NB);
-    const int my_tiles =
-        (int)blockIdx.x < args.num_tiles ? (args.num_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    const uint32_t total_steps = (uint32_t)my_tiles * KS;
-    auto load_b = [&](uint32_t step) {  // B operand of global K-step `step` into its ring slot
-      if (step >= total_steps) return;
-      const uint32_t slot = step % NBS;
+  if (warp == T::PWARPS + 1) {
+    // ================= loader warp =================
+    auto load_b = [&](int i) {  // B operand of the i-th K-step (in this CTA's order) into its ring slot
+      if (i >= KS) return;
+      const int slot = i % NBS;
+      const int step = (i + rot) % KS;
       mbar_expect_tx(&b_full[slot], T::B_STEP_BYTES);
-      bulk_g2s(s_b + slot * T::B_STEP_BYTES, args.bpack + (size_t)(step % KS) * (T::B_STEP_BYTES / 4),
-               T::B_STEP_BYTES, &b_full[slot]);
+      bulk_g2s(s_b + slot * T::B_STEP_BYTES, args.bpack + (size_t)step * (T::B_STEP_BYTES / 4), T::B_STEP_BYTES,
+               &b_full[slot]);
     };
     if (elect_one()) {
-      load_b(0);
-      load_b(1);
-    }
-    __syncwarp();
-    uint32_t g = 0;  // global K-step counter
-    int it = 0;
-    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
-      const int64_t e0 = a.e_begin + (int64_t)tile * TE;
-      const int nv = (int)min((int64_t)TE, a.e_end - e0);
+      for (int i = 0; i < T::BAHEAD; ++i) load_b(i);
       const uint32_t rowbytes = (uint32_t)nv * NPG * 4;
-      // ---- this tile's rows: geometry/connectivity once the K-loop of the previous tile is done,
-      //      each field slab once the previous tile's epilogue released it ----
-      if (it > 0) mbar_wait(tile_free, (it - 1) & 1);
-      if (elect_one()) {
-        const uint32_t geobytes = (uint32_t)nv * GEO_WORDS * 4, conbytes = (uint32_t)nv * 16;
-        mbar_expect_tx(load_full, 6 * rowbytes + geobytes + 2 * conbytes);
-        bulk_g2s(s_geo, a.geo + e0 * GEO_WORDS, geobytes, load_full);
-        bulk_g2s(s_nbr, a.nbr + e0 * 4, conbytes, load_full);
-        bulk_g2s(s_code, a.code + e0 * 4, conbytes, load_full);
-      }
-      __syncwarp();
-      for (int f = 0; f < 6; ++f) {
-        if (it > 0) mbar_wait(&slab_free[f], (it - 1) & 1);
-        if (elect_one()) bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowbytes, load_full);
-        __syncwarp();
-      }
-      if (it < 4) TC_TRACE(1, 1000 * it + 400);  // tile loads issued
-      if (elect_one()) {
-        if (MODE == MODE_LSRK && !a.a_zero)
-          for (int f = 0; f < 6; ++f) prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rowbytes);
-        const int nt = tile + gridDim.x;  // warm L2 with the next tile of this CTA
-        if (nt < args.num_tiles) {
-          const int64_t n0 = a.e_begin + (int64_t)nt * TE;
-          const uint32_t nn = (uint32_t)min((int64_t)TE, a.e_end - n0);
-          for (int f = 0; f < 6; ++f) prefetch_l2(a.u + (int64_t)f * fstride + n0 * NPG, nn * NPG * 4);
-          prefetch_l2(a.geo + n0 * GEO_WORDS, nn * GEO_WORDS * 4);
-          prefetch_l2(a.nbr + n0 * 4, nn * 16);
-          prefetch_l2(a.code + n0 * 4, nn * 16);
-        }
-      }
-      __syncwarp();
-      // ---- K loop: B ring two steps ahead, one MMA burst per step ----
-      for (int s = 0; s < KS; ++s, ++g) {
-        const int slot = g & 1;
-        if (g >= 2) mbar_wait(&empty[slot], ((g - 2) >> 1) & 1);  // MMA(g-2) done: its B slot is free
-        if (elect_one()) load_b(g + 2);
-        __syncwarp();
-        mbar_wait(&b_full[g % NBS], (g / NBS) & 1);
-        mbar_wait(&full[slot], (g >> 1) & 1);
-        if (it < 4) TC_TRACE(1, 1000 * it + 500 + 2 * s);  // stage full
-        fence_after_sync();
-        if (elect_one()) {
-          const uint32_t bh = smem_u32(s_b + (g % NBS) * T::B_STEP_BYTES);
-          const uint64_t dbh = desc_kmajor(bh, NB * 16, 128);
-          const uint64_t dbl = desc_kmajor(bh + 2 * NB * 16, NB * 16, 128);
-          const uint32_t abase = tmem + T::A_COL0 + slot * T::A_STAGE_COLS;
-          const uint32_t acc0 = s > 0 ? 1u : 0u;
-          // pass-major order: consecutive MMAs hit different accumulators
-#pragma unroll
-          for (int c = 0; c < 6; ++c) mma_tf32_ts(tmem + c * NB, abase + c * 16, dbh, idesc, acc0);
-#pragma unroll
-          for (int c = 0; c < 6; ++c) mma_tf32_ts(tmem + c * NB, abase + c * 16 + 8, dbh, idesc, 1u);
-#pragma unroll
-          for (int c = 0; c < 6; ++c) mma_tf32_ts(tmem + c * NB, abase + c * 16, dbl, idesc, 1u);
-          mma_commit(&empty[slot]);
-          if (s == KS - 1) mma_commit(acc_full);
-        }
-        __syncwarp();
-      }
+      const uint32_t geobytes = (uint32_t)nv * GEO_WORDS * 4, conbytes = (uint32_t)nv * 16;
+      mbar_expect_tx(load_full, 6 * rowbytes + geobytes + 2 * conbytes);
+      bulk_g2s(s_geo, a.geo + e0 * GEO_WORDS, geobytes, load_full);
+      bulk_g2s(s_nbr, a.nbr + e0 * 4, conbytes, load_full);
+      bulk_g2s(s_code, a.code + e0 * 4, conbytes, load_full);
+      for (int f = 0; f < 6; ++f)
+        bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowbytes, load_full);
+      if (MODE == MODE_LSRK && !a.a_zero)
+        for (int f = 0; f < 6; ++f) prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rowbytes);
     }
-    if (elect_one()) bulk_wait<0>();
     __syncwarp();
+    for (int s = 2; s + T::BAHEAD - 2 < KS; ++s) {  // refill the slot of K-step s-2 once its MMAs are done
+      mbar_wait(&empty[s & 1], ((s - 2) >> 1) & 1);
+      if (elect_one()) load_b(s + T::BAHEAD - 2);
+      __syncwarp();
+    }
+  } else if (warp == T::PWARPS) {
+    // ================= MMA warp =================
+    const uint32_t idesc = idesc_tf32(128, NB);
+    for (int s = 0; s < KS; ++s) {  // s: position in this CTA's K order
+      const int slot = s & 1;
+      mbar_wait(&b_full[s % NBS], (s / NBS) & 1);
+      TC_TRACE(1, 700 + s);  // B(s) landed
+      mbar_wait(&full[slot], (s >> 1) & 1);
+      TC_TRACE(1, 500 + 2 * s);  // stage full
+      fence_after_sync();
+      if (elect_one()) {
+        const uint32_t bh = smem_u32(s_b + (s % NBS) * T::B_STEP_BYTES);
+        const uint64_t dbh = desc_kmajor(bh, NB * 16, 128);
+        const uint64_t dbl = desc_kmajor(bh + 2 * NB * 16, NB * 16, 128);
+        const uint32_t abase = tmem + T::A_COL0 + slot * T::A_STAGE_COLS;
+        const uint32_t acc0 = s > 0 ? 1u : 0u;
+        // pass-major order: consecutive MMAs hit different accumulators
+#pragma unroll
+        for (int t = 0; t < MT; ++t) mma_tf32_ts(tmem + t * NB, abase + t * 16, dbh, idesc, acc0);
+#pragma unroll
+        for (int t = 0; t < MT; ++t) mma_tf32_ts(tmem + t * NB, abase + t * 16 + 8, dbh, idesc, 1u);
+#pragma unroll
+        for (int t = 0; t < MT; ++t) mma_tf32_ts(tmem + t * NB, abase + t * 16, dbl, idesc, 1u);
+        mma_commit(&empty[slot]);
+        if (s == KS - 1) mma_commit(acc_full);
+      }
+      __syncwarp();
+      TC_TRACE(1, 501 + 2 * s);  // issued
+    }
   } else {
     // ================= producers =================
     const int quad = warp & 3;               // TMEM lane quadrant
-    const int khalf = (warp >> 2) & 1;       // which 4 of a K step's 8 columns
-    const int grp = (warp >> 3) & 1;         // 0: E components (from H fields), 1: H components (from E fields)
-    const int egrp = warp >> 2;              // epilogue: TMEM -> smem mover for components egrp, egrp + 4
-    const int row = quad * 32 + lane;        // element row = TMEM lane
+    const int khalf = warp >> 2;             // which 4 of a K step's 8 columns
+    const int h = quad >> 1;                 // 0: E components (from H fields), 1: H components (from E fields)
+    const int row = (quad & 1) * 32 + lane;  // element row of this TMEM lane
     const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
-    const float inv_m = grp == 0 ? a.inv_eps : a.inv_mu;
-    constexpr int RV = NPG / 4;              // 16-byte chunks per row
-    constexpr int PER = (TE * RV + PROD - 1) / PROD;
-    uint32_t pstep = 0;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < args.num_tiles; tile += gridDim.x, ++it) {
-      const int64_t e0 = a.e_begin + (int64_t)tile * TE;
-      const int nv = (int)min((int64_t)TE, a.e_end - e0);
-      if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 1);  // tile start
-      mbar_wait(load_full, it & 1);
-      if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 2);  // rows landed
-
-      {  // warm L2 with the rows of every face neighbour outside the tile (read by the face K-steps)
-        const int e = tid;  // one (row, face) entry per producer thread
-        if (e < nv * 4) {
-          const int code = s_code[e];
-          const int64_t nb = s_nbr[e];
-          if (code >= 0 && (nb < e0 || nb >= e0 + nv)) {
+    const float inv_m = h == 0 ? a.inv_eps : a.inv_mu;
+    if (tid == 0) TC_TRACE(0, 1);  // start
+    mbar_wait(load_full, 0);
+    if (tid == 0) TC_TRACE(0, 2);  // rows landed
+    {  // warm L2 with the rows of every face neighbour outside the tile (read by the face K-steps)
+      for (int e = tid; e < nv * 4; e += PROD) {
+        const int code = s_code[e];
+        const int64_t nb = s_nbr[e];
+        if (code >= 0 && (nb < e0 || nb >= e0 + nv)) {
 #pragma unroll
-            for (int f = 0; f < 6; ++f) {
-              const float* p = a.u + (int64_t)f * fstride + nb * NPG;
-              prefetch_line_l2(p);
-              prefetch_line_l2(p + NPG - 1);
-            }
+          for (int f = 0; f < 6; ++f) {
+            const float* p = a.u + (int64_t)f * fstride + nb * NPG;
+            prefetch_line_l2(p);
+            prefetch_line_l2(p + NPG - 1);
           }
         }
       }
-      const bool row_ok = row < nv;
-      float prx[9];  // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu
+    }
+    const bool row_ok = row < nv;
+    float prx[9];  // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu
 #pragma unroll
-      for (int q = 0; q < 9; ++q) prx[q] = row_ok ? s_geo[row * GEO_WORDS + q] * inv_m : 0.f;
+    for (int q = 0; q < 9; ++q) prx[q] = row_ok ? s_geo[row * GEO_WORDS + q] * inv_m : 0.f;
 
-      for (int s = 0; s < KS; ++s, ++pstep) {
-        const int slot = pstep & 1;
-        const int k0 = s * 8;
-        if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 100 + 4 * s);  // step begin
-        // ---- surface flux of a whole face at its first K-step ----
-        if (k0 >= KV && (k0 - KV) % NFPK == 0) {
-          const int face = (k0 - KV) / NFPK;
-          named_sync(1, PROD);  // every thread finished reading the previous face's staging
-          float up[ITEMS][6];
+    for (int i = 0; i < KS; ++i) {  // i: position in this CTA's K order, s: K-step
+      const int slot = i & 1;
+      const int s = (i + rot) % KS;
+      const int k0 = s * 8;
+      if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
+      // ---- surface flux of a whole face at its first K-step ----
+      if (k0 >= KV && (k0 - KV) % NFPK == 0) {
+        const int face = (k0 - KV) / NFPK;
+        named_sync(1, PROD);  // every thread finished reading the previous face's staging
+        float up[ITEMS][6];
 #pragma unroll
-          for (int i = 0; i < ITEMS; ++i) {  // u+ gathers first: all loads in flight together
-            const int item = tid + i * PROD;
-            const int r = item / NFPK, node = item % NFPK;
-            const bool live = node < NFP && r < nv;
-            const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
-            const float* src = s_u + r * NPG + im;  // PEC walls mirror the own trace below
-            int64_t fs = TE * NPG;
-            const int code = live ? s_code[r * 4 + face] : -1;
-            if (code >= 0) {
-              const int nb = s_nbr[r * 4 + face];
-              const int jn = s_ptab[code * NFP + node];
-              const int64_t loc = (int64_t)nb - e0;
-              if (loc >= 0 && loc < nv) {
-                src = s_u + (int)loc * NPG + jn;
-              } else {
-                src = a.u + (int64_t)nb * NPG + jn;
-                fs = fstride;
-              }
+        for (int i = 0; i < ITEMS; ++i) {  // u+ gathers first: all loads in flight together
+          const int item = tid + i * PROD;
+          const int r = item / NFPK, node = item % NFPK;
+          const bool live = node < NFP && r < nv;
+          const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
+          const float* src = s_u + r * NPG + im;  // PEC walls mirror the own trace below
+          int64_t fs = TE * NPG;
+          const int code = live ? s_code[r * 4 + face] : -1;
+          if (code >= 0) {
+            const int nb = s_nbr[r * 4 + face];
+            const int jn = s_ptab[code * NFP + node];
+            const int64_t loc = (int64_t)nb - e0;
+            if (loc >= 0 && loc < nv) {
+              src = s_u + (int)loc * NPG + jn;
+            } else {
+              src = a.u + (int64_t)nb * NPG + jn;
+              fs = fstride;
             }
-#pragma unroll
-            for (int f = 0; f < 6; ++f) up[i][f] = src[f * fs];
           }
 #pragma unroll
-          for (int i = 0; i < ITEMS; ++i) {
-            const int item = tid + i * PROD;
-            const int r = item / NFPK, node = item % NFPK;
-            const bool live = node < NFP && r < nv;
-            const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
-            float um[6];
+          for (int f = 0; f < 6; ++f) up[i][f] = src[f * fs];
+        }
 #pragma unroll
-            for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + r) * NPG + im];
-            const float* gk = s_geo + r * GEO_WORDS;
-            const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
-            if (live && s_code[r * 4 + face] < 0) {  // PEC mirror (maxwell.py:117-132)
-              const float nde = nx * um[0] + ny * um[1] + nz * um[2];
-              const float ndh = nx * um[3] + ny * um[4] + nz * um[5];
-              up[i][0] = -um[0] + 2.f * nde * nx;
-              up[i][1] = -um[1] + 2.f * nde * ny;
-              up[i][2] = -um[2] + 2.f * nde * nz;
-              up[i][3] = um[3] - 2.f * ndh * nx;
-              up[i][4] = um[4] - 2.f * ndh * ny;
-              up[i][5] = um[5] - 2.f * ndh * nz;
-            }
-            float out[6];
-            upwind(um, up[i], nx, ny, nz, a, out);
-            const float sc = live ? gk[22 + face] * gk[9] : 0.f;
-            const float se = sc * a.inv_eps, sh = sc * a.inv_mu;
+        for (int i = 0; i < ITEMS; ++i) {
+          const int item = tid + i * PROD;
+          const int r = item / NFPK, node = item % NFPK;
+          const bool live = node < NFP && r < nv;
+          const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
+          float um[6];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * se;
-#pragma unroll
-            for (int c = 3; c < 6; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * sh;
+          for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + r) * NPG + im];
+          const float* gk = s_geo + r * GEO_WORDS;
+          const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
+          if (live && s_code[r * 4 + face] < 0) {  // PEC mirror (maxwell.py:117-132)
+            const float nde = nx * um[0] + ny * um[1] + nz * um[2];
+            const float ndh = nx * um[3] + ny * um[4] + nz * um[5];
+            up[i][0] = -um[0] + 2.f * nde * nx;
+            up[i][1] = -um[1] + 2.f * nde * ny;
+            up[i][2] = -um[2] + 2.f * nde * nz;
+            up[i][3] = um[3] - 2.f * ndh * nx;
+            up[i][4] = um[4] - 2.f * ndh * ny;
+            up[i][5] = um[5] - 2.f * ndh * nz;
           }
-          named_sync(1, PROD);
-          if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 103 + 4 * s);  // face flux staged
+          float out[6];
+          upwind(um, up[i], nx, ny, nz, a, out);
+          const float sc = live ? gk[22 + face] * gk[9] : 0.f;
+          const float se = sc * a.inv_eps, sh = sc * a.inv_mu;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * se;
+#pragma unroll
+          for (int c = 3; c < 6; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * sh;
         }
-
-        // ---- A K-step (this warp's 4 columns, 3 components) into TMEM, thread-per-row ----
-        float v[3][4];
-        {
-          const int k = k0 + 4 * khalf;
-          if (k < 3 * NPK) {
-            const int mu = k / NPK, j0 = k - mu * NPK;
-            const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
-            const int fb = grp == 0 ? 3 : 0;  // E comps read H fields and vice versa
-            const float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + 0) * TE + row) * NPG + j0);
-            const float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + 1) * TE + row) * NPG + j0);
-            const float4 z = *reinterpret_cast<const float4*>(s_u + ((fb + 2) * TE + row) * NPG + j0);
-            const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w}, zs[4] = {z.x, z.y, z.z, z.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (grp == 0) {  // (curl H)_x,y,z
-                v[0][q] = p1 * zs[q] - p2 * ys[q];
-                v[1][q] = p2 * xs[q] - p0 * zs[q];
-                v[2][q] = p0 * ys[q] - p1 * xs[q];
-              } else {         // -(curl E)_x,y,z
-                v[0][q] = p2 * ys[q] - p1 * zs[q];
-                v[1][q] = p0 * zs[q] - p2 * xs[q];
-                v[2][q] = p1 * xs[q] - p0 * ys[q];
-              }
-            }
-          } else if (k >= KV) {
-            const int node = (k - KV) % NFPK;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-              for (int c = 0; c < 3; ++c) v[c][q] = s_stage[((3 * grp + c) * NFPK + node + q) * SROW + row];
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-              for (int c = 0; c < 3; ++c) v[c][q] = 0.f;
-          }
-        }
-        float hi[3][4], lo[3][4];
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) split_tf32(row_ok ? v[c][q] : 0.f, hi[c][q], lo[c][q]);
-        if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 101 + 4 * s);  // A values ready
-        mbar_wait(&empty[slot], ((pstep >> 1) & 1) ^ 1);
-        if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 102 + 4 * s);  // stage free
-        fence_after_sync();
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + (3 * grp + c) * 16 + 4 * khalf;
-          tmem_st4(tmem + lane_addr + col, hi[c]);
-          tmem_st4(tmem + lane_addr + col + 8, lo[c]);
-        }
-        tmem_st_wait();
-        fence_before_sync();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&full[slot]);
-          if (s == KS - 1) mbar_arrive(tile_free);  // geometry / connectivity may be refilled
-        }
+        named_sync(1, PROD);
+        if (tid == 0) TC_TRACE(0, 103 + 4 * s);  // face flux staged
       }
 
-      // ================= epilogue: accumulators -> LSRK update =================
-      if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 3);  // all steps produced
-      mbar_wait(acc_full, it & 1);
-      if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 4);  // accumulators final
+      // ---- A K-step (this thread's 4 columns of its row in the 3 M-tiles) ----
+      float v[MT][4];
+      {
+        const int k = k0 + 4 * khalf;
+        if (k < 3 * NPK) {
+          const int mu = k / NPK, j0 = k - mu * NPK;
+          const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
+          const int fb = h == 0 ? 3 : 0;  // E comps read H fields and vice versa
+          const float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + 0) * TE + row) * NPG + j0);
+          const float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + 1) * TE + row) * NPG + j0);
+          const float4 z = *reinterpret_cast<const float4*>(s_u + ((fb + 2) * TE + row) * NPG + j0);
+          const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w}, zs[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (h == 0) {  // (curl H)_x,y,z
+              v[0][q] = p1 * zs[q] - p2 * ys[q];
+              v[1][q] = p2 * xs[q] - p0 * zs[q];
+              v[2][q] = p0 * ys[q] - p1 * xs[q];
+            } else {       // -(curl E)_x,y,z
+              v[0][q] = p2 * ys[q] - p1 * zs[q];
+              v[1][q] = p0 * zs[q] - p2 * xs[q];
+              v[2][q] = p1 * xs[q] - p0 * ys[q];
+            }
+          }
+        } else if (k >= KV) {
+          const int node = (k - KV) % NFPK;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int t = 0; t < MT; ++t) v[t][q] = s_stage[((3 * h + t) * NFPK + node + q) * SROW + row];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int t = 0; t < MT; ++t) v[t][q] = 0.f;
+        }
+      }
+      float hi[MT][4], lo[MT][4];
+#pragma unroll
+      for (int t = 0; t < MT; ++t)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) split_tf32(row_ok ? v[t][q] : 0.f, hi[t][q], lo[t][q]);
+      if (tid == 0) TC_TRACE(0, 101 + 4 * s);  // A values ready
+      mbar_wait(&empty[slot], ((i >> 1) & 1) ^ 1);
+      if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free
       fence_after_sync();
-      // TMEM -> smem rows buffer (thread-per-row), done by one quadrant-complete warp group
-      auto move_acc = [&](int comp) {
-        float* dst = s_stage + (size_t)(comp & 1) * TE * NPG + row * NPG;
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + t * 16 + 4 * khalf;
+        tmem_st4(tmem + lane_addr + col, hi[t]);
+        tmem_st4(tmem + lane_addr + col + 8, lo[t]);
+      }
+      tmem_st_wait();
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[slot]);
+    }
+
+    // ================= epilogue: accumulators -> LSRK update =================
+    if (tid == 0) TC_TRACE(0, 3);  // all steps produced
+    constexpr int RV = NPG / 4;    // 16-byte chunks per row
+    const int nvec = nv * RV;      // chunks per component slab
+    constexpr int PER = (2 * TE * RV + PROD - 1) / PROD;
+    mbar_wait(acc_full, 0);
+    if (tid == 0) TC_TRACE(0, 4);  // accumulators final
+    fence_after_sync();
+#pragma unroll 1
+    for (int t = 0; t < MT; ++t) {
+      // residual rows of components t and t+3 (L2-prefetched at CTA start), all loads in flight
+      float4 ro[PER];
+#pragma unroll
+      for (int p = 0; p < PER; ++p) {
+        const int idx = tid + p * PROD;
+        const int which = idx >= nvec ? 1 : 0;
+        const int c = idx - which * nvec;
+        ro[p] = (MODE == MODE_LSRK && !a.a_zero && c < nvec)
+                    ? __ldcs(reinterpret_cast<const float4*>(a.res + ((int64_t)(t + 3 * which) * a.kf + e0) * NPG) + c)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (khalf == 0) {  // quadrant warps: TMEM lanes -> smem rows [E_t | H_t][row][NPG]
+        float* dst = s_stage + (size_t)h * TE * NPG + row * NPG;
 #pragma unroll
         for (int c0 = 0; c0 < NB; c0 += 8) {
           float r8[8];
-          tmem_ld8(tmem + lane_addr + comp * NB + c0, r8);
+          tmem_ld8(tmem + lane_addr + t * NB + c0, r8);
           tmem_ld_wait();
 #pragma unroll
           for (int q = 0; q < 8; q += 4) {
@@ -446,61 +428,39 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 1) tc_stage_kernel(const Tc
             }
           }
         }
-      };
-      const int nvec = nv * RV;
-      auto load_res = [&](int comp, float4* ro) {
-#pragma unroll
-        for (int p = 0; p < PER; ++p) {
-          const int c = tid + p * PROD;
-          ro[p] = (MODE == MODE_LSRK && !a.a_zero && c < nvec)
-                      ? __ldcs(reinterpret_cast<const float4*>(a.res + ((int64_t)comp * a.kf + e0) * NPG) + c)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      };
-      float4 ro[PER], rn[PER];
-      if (egrp == 0) move_acc(0);
-      load_res(0, ro);
+      }
       named_sync(1, PROD);
-#pragma unroll 1
-      for (int comp = 0; comp < 6; ++comp) {
-        if (comp + 1 < 6) {
-          if (egrp == ((comp + 1) & 3)) move_acc(comp + 1);
-          load_res(comp + 1, rn);
-        }
-        const float4* rs = reinterpret_cast<const float4*>(s_stage + (size_t)(comp & 1) * TE * NPG);
-        const float4* us = reinterpret_cast<const float4*>(s_u + (size_t)comp * TE * NPG);
-        const int64_t gbase = ((int64_t)comp * a.kf + e0) * NPG;
 #pragma unroll
-        for (int p = 0; p < PER; ++p) {
-          const int c = tid + p * PROD;
-          if (c < nvec) {
-            const float4 rh = rs[c];
-            if (MODE == MODE_RHS) {
-              *reinterpret_cast<float4*>(a.out + gbase + (int64_t)c * 4) = rh;
+      for (int p = 0; p < PER; ++p) {
+        const int idx = tid + p * PROD;
+        const int which = idx >= nvec ? 1 : 0;
+        const int c = idx - which * nvec;
+        if (c < nvec) {
+          const int comp = t + 3 * which;
+          const int64_t gbase = ((int64_t)comp * a.kf + e0) * NPG;
+          const float4 rh = reinterpret_cast<const float4*>(s_stage + (size_t)which * TE * NPG)[c];
+          if (MODE == MODE_RHS) {
+            *reinterpret_cast<float4*>(a.out + gbase + (int64_t)c * 4) = rh;
+          } else {
+            float4 r;
+            if (a.a_zero) {
+              r = make_float4(a.dt * rh.x, a.dt * rh.y, a.dt * rh.z, a.dt * rh.w);
             } else {
-              float4 r;
-              if (a.a_zero) {
-                r = make_float4(a.dt * rh.x, a.dt * rh.y, a.dt * rh.z, a.dt * rh.w);
-              } else {
-                r = make_float4(a.a * ro[p].x + a.dt * rh.x, a.a * ro[p].y + a.dt * rh.y,
-                                a.a * ro[p].z + a.dt * rh.z, a.a * ro[p].w + a.dt * rh.w);
-              }
-              const float4 uo = us[c];
-              __stcs(reinterpret_cast<float4*>(a.res + gbase) + c, r);
-              __stcs(reinterpret_cast<float4*>(a.u_out + gbase) + c,
-                     make_float4(uo.x + a.b * r.x, uo.y + a.b * r.y, uo.z + a.b * r.z, uo.w + a.b * r.w));
+              r = make_float4(a.a * ro[p].x + a.dt * rh.x, a.a * ro[p].y + a.dt * rh.y,
+                              a.a * ro[p].z + a.dt * rh.z, a.a * ro[p].w + a.dt * rh.w);
             }
+            const float4 uo = reinterpret_cast<const float4*>(s_u + (size_t)comp * TE * NPG)[c];
+            __stcs(reinterpret_cast<float4*>(a.res + gbase) + c, r);
+            __stcs(reinterpret_cast<float4*>(a.u_out + gbase) + c,
+                   make_float4(uo.x + a.b * r.x, uo.y + a.b * r.y, uo.z + a.b * r.z, uo.w + a.b * r.w));
           }
         }
-        named_sync(1, PROD);  // rows buffer `comp & 1` and field slab `comp` fully read
-        if (tid == 0) mbar_arrive(&slab_free[comp]);
-#pragma unroll
-        for (int p = 0; p < PER; ++p) ro[p] = rn[p];
       }
-      if (tid == 0 && it < 4) TC_TRACE(0, 1000 * it + 5);  // epilogue done
-      fence_before_sync();
+      named_sync(1, PROD);  // rows buffer free for the next M-tile
     }
+    if (tid == 0) TC_TRACE(0, 5);  // epilogue done
   }
+  fence_before_sync();
   __syncthreads();
   fence_after_sync();
   if (warp == 0) tmem_dealloc(tmem, T::TMEM_COLS);

@@ -102,23 +102,25 @@ __device__ __forceinline__ void mbar_arrive(void* mbar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
 }
 
-#ifdef DGM_TC_TRACE
-__device__ unsigned int g_hang[8];
-__device__ __forceinline__ bool mbar_try(void* mbar, uint32_t parity) {
+// Non-suspending probe of an mbarrier phase.
+__device__ __forceinline__ bool mbar_test(void* mbar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, P1;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(mbar)), "r"(parity)
       : "memory");
   return ok != 0;
 }
+
+#ifdef DGM_TC_TRACE
+__device__ unsigned int g_hang[8];
 // Trace build: a wait that never completes records who/what and traps.
 __device__ __noinline__ void mbar_wait(void* mbar, uint32_t parity) {
-  for (uint32_t i = 0; !mbar_try(mbar, parity); ++i) {
-    if (i == (1u << 22)) {
+  for (uint32_t i = 0; !mbar_test(mbar, parity); ++i) {
+    if (i == (1u << 26)) {
       if (atomicCAS(&g_hang[0], 0u, 1u) == 0u) {
         g_hang[1] = blockIdx.x;
         g_hang[2] = threadIdx.x;
@@ -131,16 +133,11 @@ __device__ __noinline__ void mbar_wait(void* mbar, uint32_t parity) {
   }
 }
 #else
+// Spin on test_wait: try_wait's suspend / wake-up costs ~0.5k cycles per hand-off, which is
+// the whole budget of a K-step pipeline stage here.
 __device__ __forceinline__ void mbar_wait(void* mbar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n\t"
-      "DONE_%=:\n\t}" ::"r"(smem_u32(mbar)),
-      "r"(parity), "r"(0x989680u)
-      : "memory");
+  while (!mbar_test(mbar, parity)) {
+  }
 }
 #endif
 

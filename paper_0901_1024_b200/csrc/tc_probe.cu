@@ -229,6 +229,132 @@ __global__ void __launch_bounds__(128) probe_rate_kernel(int n, int reps, int ts
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
 }
 
+// Round-trip latency of the stage kernel's MMA pattern: one elected lane issues a burst of
+// `nacc` x `passes` TS MMAs (M=128, N=n, K=8, accumulators round-robin), commits to an mbarrier
+// and waits for it; repeated `reps` times.  cycles[0] = total, cycles[1] = issue part.
+__global__ void __launch_bounds__(128) probe_burst_kernel(int n, int reps, int nacc, int passes, long long* cycles) {
+  using namespace dgm::tc;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  float* b_s = reinterpret_cast<float*>(smem);  // n x 8
+  for (int i = threadIdx.x; i < n * 8; i += blockDim.x) b_s[i] = 0.f;
+  if (threadIdx.x < 32) tmem_alloc(&tmem_base, 256);
+  if (threadIdx.x == 32) {
+    mbar_init(&mbar, 1);
+    mbar_init_fence();
+  }
+  fence_async_smem();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  if (threadIdx.x < 32) {
+    const uint32_t idesc = idesc_tf32(128, n);
+    const uint64_t bd = desc_kmajor(smem_u32(b_s), n * 16, 128);
+    long long issue = 0;
+    __syncwarp();
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const long long ti = clock64();
+      if (elect_one()) {
+        for (int p = 0; p < passes; ++p)
+          for (int c = 0; c < nacc; ++c) mma_tf32_ts(tmem + (uint32_t)(c * n), tmem + 224, bd, idesc, 1u);
+        mma_commit(&mbar);
+      }
+      __syncwarp();
+      issue += clock64() - ti;
+      mbar_wait(&mbar, r & 1);
+      fence_after_sync();
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) {
+      cycles[0] = t1 - t0;
+      cycles[1] = issue;
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 256);
+}
+
+// Primitive costs of the stage kernel's producer / MMA hand-off (one CTA, `pw` producer warps + 1 MMA warp):
+//   mode 0: producers only, per iteration 6 x tcgen05.st.32x32b.x4 + wait::st (no MMA)
+//   mode 1: full ping-pong with a 2-stage A ring: producers wait empty, store, fence, arrive full;
+//           the MMA warp waits full, issues 9 TS MMAs (3 accumulators x 3 passes), commits empty.
+// cycles[0] = total cycles of producer warp 0 for `reps` iterations.
+__global__ void __launch_bounds__(320) probe_handoff_kernel(int reps, int mode, int pw, long long* cycles) {
+  using namespace dgm::tc;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ uint32_t tmem_base;
+  float* b_s = reinterpret_cast<float*>(smem);  // 48 x 8 x 2
+  for (int i = threadIdx.x; i < 48 * 16; i += blockDim.x) b_s[i] = 0.f;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) tmem_alloc(&tmem_base, 256);
+  if (threadIdx.x == 32) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], pw);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init_fence();
+  }
+  fence_async_smem();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  if (warp < pw) {
+    const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int khalf = (warp >> 2) & 1;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const int slot = r & 1;
+      if (mode == 1) {
+        mbar_wait(&empty[slot], ((r >> 1) & 1) ^ 1);
+        fence_after_sync();
+      }
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const uint32_t col = 160 + slot * 48 + t * 16 + 4 * khalf;
+        tmem_st4(tmem + lane_addr + col, v);
+        tmem_st4(tmem + lane_addr + col + 8, v);
+      }
+      tmem_st_wait();
+      if (mode == 1) {
+        fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[slot]);
+      }
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) cycles[0] = t1 - t0;
+  } else if (warp == pw && mode == 1) {
+    const uint32_t idesc = idesc_tf32(128, 48);
+    const uint64_t bd = desc_kmajor(smem_u32(b_s), 48 * 16, 128);
+    for (int r = 0; r < reps; ++r) {
+      const int slot = r & 1;
+      mbar_wait(&full[slot], (r >> 1) & 1);
+      fence_after_sync();
+      if (elect_one()) {
+        const uint32_t abase = tmem + 160 + slot * 48;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) mma_tf32_ts(tmem + t * 48, abase + t * 16, bd, idesc, r > 0);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) mma_tf32_ts(tmem + t * 48, abase + t * 16 + 8, bd, idesc, 1u);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) mma_tf32_ts(tmem + t * 48, abase + t * 16, bd, idesc, 1u);
+        mma_commit(&empty[slot]);
+      }
+      __syncwarp();
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
 }  // namespace
 
 extern "C" int dgm_probe_mma_rate(int n, int reps, int ts, int nacc, long long* cycles_dev) {
@@ -255,5 +381,18 @@ extern "C" int dgm_probe_tf32_gemm(const float* a, const float* b, float* c, int
   if (cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return -2;
   probe_kernel<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(a, b, c, n, k, passes);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int dgm_probe_mma_burst(int n, int reps, int nacc, int passes, int ctas, long long* cycles_dev) {
+  if (n % 16 || n < 16 || nacc * n > 224 || passes < 1) return -1;
+  const size_t smem = (size_t)n * 8 * 4 + 1024;
+  probe_burst_kernel<<<ctas, 128, smem>>>(n, reps, nacc, passes, cycles_dev);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int dgm_probe_handoff(int reps, int mode, int pw, int ctas, long long* cycles_dev) {
+  if (pw < 1 || pw > 8 || reps < 2) return -1;
+  probe_handoff_kernel<<<ctas, 32 * (pw + 1), 48 * 16 * 4 + 1024>>>(reps, mode, pw, cycles_dev);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

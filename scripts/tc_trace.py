@@ -4,7 +4,7 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-os.environ["DGM_LIB"] = os.path.join(ROOT, "paper_0901_1024_b200", "libdgm_trace.so")
+os.environ.setdefault("DGM_LIB", os.path.join(ROOT, "paper_0901_1024_b200", "libdgm_trace.so"))
 sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402

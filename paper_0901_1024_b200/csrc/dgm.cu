@@ -91,6 +91,8 @@ DGM_TC_INFO(1)
 DGM_TC_INFO(2)
 DGM_TC_INFO(3)
 DGM_TC_INFO(4)
+DGM_TC_INFO(5)
+DGM_TC_INFO(6)
 #undef DGM_TC_INFO
 }  // namespace
 
@@ -187,6 +189,8 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
     using T = decltype(t);
     if constexpr (TcInfo<N, T>::supported) {
       if (d.path == DGM_PATH_SIMT) return DGM_OK;
+      // AUTO: at N=1 the GEMM is too thin for the tensor cores to pay off (C2 sweep)
+      if (d.path == DGM_PATH_AUTO && N < 2) return DGM_OK;
       if (!d.tc_operand || !aligned16(d.tc_operand)) {
         if (d.path == DGM_PATH_TENSOR)
           return fail(DGM_ERR_INVALID, "tensor path requested without a 16-byte aligned tc_operand");
@@ -194,8 +198,9 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
       }
       using TC = dgm::TcCfg<N>;
       tc_smem = (TC::SMEM_FIXED + (size_t)d.num_codes * TC::NFP + 127) & ~size_t(127);
-      // at most two CTAs per SM: each allocates 256 of the 512 TMEM columns
-      if (tc_smem < 80 * 1024) tc_smem = 80 * 1024;
+      // never more CTAs per SM than TcCfg::CTAS: each allocates 512 / CTAS TMEM columns
+      if (TC::CTAS == 2 && tc_smem < 80 * 1024) tc_smem = 80 * 1024;
+      if (TC::CTAS == 1 && tc_smem < 120 * 1024) tc_smem = 120 * 1024;
       if (tc_smem > 227 * 1024) {
         if (d.path == DGM_PATH_TENSOR) return fail(DGM_ERR_UNSUPPORTED, "tensor path smem %zu too large", tc_smem);
         return DGM_OK;

@@ -88,15 +88,19 @@ struct TcCfg {
   static constexpr int ACC_COLS = MT * NB;
   static constexpr int A_COL0 = (ACC_COLS + 31) / 32 * 32;
   static constexpr int A_STAGE_COLS = MT * 16;     // 3 M-tiles x (8 hi + 8 lo)
-  static constexpr int TMEM_COLS = 256;
-  static_assert(A_COL0 + 2 * A_STAGE_COLS <= TMEM_COLS, "TMEM budget (two CTAs per SM)");
+  static constexpr int CTAS = N <= 4 ? 2 : 1;     // CTAs per SM (TMEM and smem split between them)
+  static constexpr int TMEM_COLS = 512 / CTAS;
+  static constexpr int AST0 = (TMEM_COLS - A_COL0) / A_STAGE_COLS;
+  static constexpr int AST = AST0 > 6 ? 6 : AST0;   // A ring stages in TMEM
+  static_assert(AST >= 2, "TMEM budget");
   static constexpr int SROW = TE + 4;              // flux staging row stride
   static constexpr int B_STEP_BYTES = 2 * 2 * NB * 16;   // hi/lo x 2 chunks x NB rows x 16 B
-  static constexpr int NBS = 6;                    // B ring slots
-  static constexpr int BAHEAD = NBS - 2;           // B loaded this many K-steps ahead of its MMAs
+  static constexpr int NBS = N <= 5 ? 6 : 4;       // B ring slots (a slot is refilled when its MMAs complete)
   static constexpr uint32_t ROWS_BYTES = TE * NPG * 4;   // one field slab of the tile
   static constexpr int ITEMS = TE * NFPK / PROD;   // (row, face node) flux items per thread
   static_assert(ITEMS * PROD == TE * NFPK, "flux items must tile the producers");
+  static constexpr int IB = ITEMS % 4 == 0 ? 4 : (ITEMS % 3 == 0 ? 3 : (ITEMS % 2 == 0 ? 2 : 1));  // per gather batch
+  static_assert(ITEMS % IB == 0, "flux batches");
   // shared-memory carve-up (bytes)
   static constexpr size_t OFF_U = 0;
   static constexpr size_t OFF_GEO = OFF_U + (size_t)6 * ROWS_BYTES;
@@ -107,7 +111,7 @@ struct TcCfg {
   static constexpr size_t EPI_BYTES = (size_t)2 * ROWS_BYTES;
   static constexpr size_t OFF_STAGE = OFF_B + (size_t)NBS * B_STEP_BYTES;
   static constexpr size_t OFF_BAR = OFF_STAGE + (FLUX_BYTES > EPI_BYTES ? FLUX_BYTES : EPI_BYTES);
-  static constexpr size_t OFF_FMASK = OFF_BAR + 128;  // 10 mbarriers + TMEM base address
+  static constexpr size_t OFF_FMASK = OFF_BAR + 256;  // mbarriers + TMEM base address
   static constexpr size_t OFF_PTAB = OFF_FMASK + (4 * NFP + 15) / 16 * 16;
   static constexpr size_t SMEM_FIXED = OFF_PTAB;   // + ncodes * NFP
   static constexpr size_t B_FLOATS = (size_t)KS * 2 * 2 * NB * 4;  // packed operand in global
@@ -120,12 +124,12 @@ struct TcArgs {
 };
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const TcArgs args) {
+__global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_kernel(const TcArgs args) {
   using T = TcCfg<N>;
   using namespace tc;
   constexpr int TE = T::TE, NPG = T::NPG, NP = T::NP, NFP = T::NFP, NB = T::NB, NFPK = T::NFPK;
   constexpr int KS = T::KS, KV = T::KV, NPK = T::NPK, SROW = T::SROW, PROD = T::PROD, NBS = T::NBS;
-  constexpr int ITEMS = T::ITEMS, MT = T::MT;
+  constexpr int ITEMS = T::ITEMS, IB = T::IB, MT = T::MT, AST = T::AST;
   const StageArgs<float>& a = args.s;
 
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -136,13 +140,14 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const Tc
   unsigned char* s_b = smem + T::OFF_B;
   float* s_stage = reinterpret_cast<float*>(smem + T::OFF_STAGE);  // flux of one face | epilogue rows
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::OFF_BAR);
-  uint64_t* full = bar + 0;        // [2] producers -> MMA (A stage written)
-  uint64_t* empty = bar + 2;       // [2] MMA commit -> A stage / B slot reusable
-  uint64_t* load_full = bar + 4;   // tile rows landed
-  uint64_t* acc_full = bar + 5;    // accumulators final
-  uint64_t* b_full = bar + 6;      // [NBS] B ring slot landed
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bar + 6 + NBS);
-  static_assert((6 + NBS) * 8 + 4 <= 128, "barrier region");
+  uint64_t* full = bar;            // [AST] producers -> MMA (A stage written)
+  uint64_t* empty = full + AST;    // [AST] MMA commit -> A stage reusable
+  uint64_t* b_full = empty + AST;  // [NBS] B ring slot landed
+  uint64_t* b_empty = b_full + NBS;  // [NBS] MMA commit -> B slot reusable
+  uint64_t* load_full = b_empty + NBS;  // tile rows landed
+  uint64_t* acc_full = load_full + 1;   // accumulators final
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(acc_full + 1);
+  static_assert((2 * AST + 2 * NBS + 2) * 8 + 4 <= 256, "barrier region");
   uint8_t* s_fmask = smem + T::OFF_FMASK;
   uint8_t* s_ptab = smem + T::OFF_PTAB;
 
@@ -157,13 +162,16 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const Tc
 
   if (warp == 0) tmem_alloc(s_tmem, T::TMEM_COLS);
   if (tid == PROD) {
-    mbar_init(&full[0], T::PWARPS);
-    mbar_init(&full[1], T::PWARPS);
-    mbar_init(&empty[0], 1);
-    mbar_init(&empty[1], 1);
+    for (int i = 0; i < AST; ++i) {
+      mbar_init(&full[i], T::PWARPS);
+      mbar_init(&empty[i], 1);
+    }
     mbar_init(load_full, 1);
     mbar_init(acc_full, 1);
-    for (int i = 0; i < NBS; ++i) mbar_init(&b_full[i], 1);
+    for (int i = 0; i < NBS; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
     mbar_init_fence();
   }
   for (int c = tid; c < 4 * NFP; c += blockDim.x) s_fmask[c] = a.fmask[c];
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const Tc
                &b_full[slot]);
     };
     if (elect_one()) {
-      for (int i = 0; i < T::BAHEAD; ++i) load_b(i);
+      for (int i = 0; i < NBS; ++i) load_b(i);
       const uint32_t rowbytes = (uint32_t)nv * NPG * 4;
       const uint32_t geobytes = (uint32_t)nv * GEO_WORDS * 4, conbytes = (uint32_t)nv * 16;
       mbar_expect_tx(load_full, 6 * rowbytes + geobytes + 2 * conbytes);
@@ -198,19 +206,21 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const Tc
         for (int f = 0; f < 6; ++f) prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rowbytes);
     }
     __syncwarp();
-    for (int s = 2; s + T::BAHEAD - 2 < KS; ++s) {  // refill the slot of K-step s-2 once its MMAs are done
-      mbar_wait(&empty[s & 1], ((s - 2) >> 1) & 1);
-      if (elect_one()) load_b(s + T::BAHEAD - 2);
+    // Refill B slot j % NBS with K-step j + NBS once the MMAs of step j completed.  b_empty[slot]
+    // cannot run a phase ahead of this wait: its next completion needs B(j + NBS), loaded below.
+    for (int j = 0; j + NBS < KS; ++j) {
+      mbar_wait(&b_empty[j % NBS], (j / NBS) & 1);
+      if (elect_one()) load_b(j + NBS);
       __syncwarp();
     }
   } else if (warp == T::PWARPS) {
     // ================= MMA warp =================
     const uint32_t idesc = idesc_tf32(128, NB);
     for (int s = 0; s < KS; ++s) {  // s: position in this CTA's K order
-      const int slot = s & 1;
+      const int slot = s % AST;
       mbar_wait(&b_full[s % NBS], (s / NBS) & 1);
       TC_TRACE(1, 700 + s);  // B(s) landed
-      mbar_wait(&full[slot], (s >> 1) & 1);
+      mbar_wait(&full[slot], (s / AST) & 1);
       TC_TRACE(1, 500 + 2 * s);  // stage full
       fence_after_sync();
       if (elect_one()) {
@@ -227,6 +237,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const Tc
 #pragma unroll
         for (int t = 0; t < MT; ++t) mma_tf32_ts(tmem + t * NB, abase + t * 16, dbl, idesc, 1u);
         mma_commit(&empty[slot]);
+        mma_commit(&b_empty[s % NBS]);
         if (s == KS - 1) mma_commit(acc_full);
       }
       __syncwarp();
@@ -263,7 +274,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const Tc
     for (int q = 0; q < 9; ++q) prx[q] = row_ok ? s_geo[row * GEO_WORDS + q] * inv_m : 0.f;
 
     for (int i = 0; i < KS; ++i) {  // i: position in this CTA's K order, s: K-step
-      const int slot = i & 1;
+      const int slot = i % AST;
       const int s = (i + rot) % KS;
       const int k0 = s * 8;
       if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
@@ -271,59 +282,62 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const Tc
       if (k0 >= KV && (k0 - KV) % NFPK == 0) {
         const int face = (k0 - KV) / NFPK;
         named_sync(1, PROD);  // every thread finished reading the previous face's staging
-        float up[ITEMS][6];
+#pragma unroll 1
+        for (int ib = 0; ib < ITEMS; ib += IB) {
+          float up[IB][6];
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {  // u+ gathers first: all loads in flight together
-          const int item = tid + i * PROD;
-          const int r = item / NFPK, node = item % NFPK;
-          const bool live = node < NFP && r < nv;
-          const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
-          const float* src = s_u + r * NPG + im;  // PEC walls mirror the own trace below
-          int64_t fs = TE * NPG;
-          const int code = live ? s_code[r * 4 + face] : -1;
-          if (code >= 0) {
-            const int nb = s_nbr[r * 4 + face];
-            const int jn = s_ptab[code * NFP + node];
-            const int64_t loc = (int64_t)nb - e0;
-            if (loc >= 0 && loc < nv) {
-              src = s_u + (int)loc * NPG + jn;
-            } else {
-              src = a.u + (int64_t)nb * NPG + jn;
-              fs = fstride;
+          for (int i = 0; i < IB; ++i) {  // u+ gathers first: a batch of loads in flight together
+            const int item = tid + (ib + i) * PROD;
+            const int r = item / NFPK, node = item % NFPK;
+            const bool live = node < NFP && r < nv;
+            const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
+            const float* src = s_u + r * NPG + im;  // PEC walls mirror the own trace below
+            int64_t fs = TE * NPG;
+            const int code = live ? s_code[r * 4 + face] : -1;
+            if (code >= 0) {
+              const int nb = s_nbr[r * 4 + face];
+              const int jn = s_ptab[code * NFP + node];
+              const int64_t loc = (int64_t)nb - e0;
+              if (loc >= 0 && loc < nv) {
+                src = s_u + (int)loc * NPG + jn;
+              } else {
+                src = a.u + (int64_t)nb * NPG + jn;
+                fs = fstride;
+              }
             }
+#pragma unroll
+            for (int f = 0; f < 6; ++f) up[i][f] = src[f * fs];
           }
 #pragma unroll
-          for (int f = 0; f < 6; ++f) up[i][f] = src[f * fs];
-        }
+          for (int i = 0; i < IB; ++i) {
+            const int item = tid + (ib + i) * PROD;
+            const int r = item / NFPK, node = item % NFPK;
+            const bool live = node < NFP && r < nv;
+            const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
+            float um[6];
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-          const int item = tid + i * PROD;
-          const int r = item / NFPK, node = item % NFPK;
-          const bool live = node < NFP && r < nv;
-          const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
-          float um[6];
+            for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + r) * NPG + im];
+            const float* gk = s_geo + r * GEO_WORDS;
+            const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
+            if (live && s_code[r * 4 + face] < 0) {  // PEC mirror (maxwell.py:117-132)
+              const float nde = nx * um[0] + ny * um[1] + nz * um[2];
+              const float ndh = nx * um[3] + ny * um[4] + nz * um[5];
+              up[i][0] = -um[0] + 2.f * nde * nx;
+              up[i][1] = -um[1] + 2.f * nde * ny;
+              up[i][2] = -um[2] + 2.f * nde * nz;
+              up[i][3] = um[3] - 2.f * ndh * nx;
+              up[i][4] = um[4] - 2.f * ndh * ny;
+              up[i][5] = um[5] - 2.f * ndh * nz;
+            }
+            float out[6];
+            upwind(um, up[i], nx, ny, nz, a, out);
+            const float sc = live ? gk[22 + face] * gk[9] : 0.f;
+            const float se = sc * a.inv_eps, sh = sc * a.inv_mu;
 #pragma unroll
-          for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + r) * NPG + im];
-          const float* gk = s_geo + r * GEO_WORDS;
-          const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
-          if (live && s_code[r * 4 + face] < 0) {  // PEC mirror (maxwell.py:117-132)
-            const float nde = nx * um[0] + ny * um[1] + nz * um[2];
-            const float ndh = nx * um[3] + ny * um[4] + nz * um[5];
-            up[i][0] = -um[0] + 2.f * nde * nx;
-            up[i][1] = -um[1] + 2.f * nde * ny;
-            up[i][2] = -um[2] + 2.f * nde * nz;
-            up[i][3] = um[3] - 2.f * ndh * nx;
-            up[i][4] = um[4] - 2.f * ndh * ny;
-            up[i][5] = um[5] - 2.f * ndh * nz;
+            for (int c = 0; c < 3; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * se;
+#pragma unroll
+            for (int c = 3; c < 6; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * sh;
           }
-          float out[6];
-          upwind(um, up[i], nx, ny, nz, a, out);
-          const float sc = live ? gk[22 + face] * gk[9] : 0.f;
-          const float se = sc * a.inv_eps, sh = sc * a.inv_mu;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * se;
-#pragma unroll
-          for (int c = 3; c < 6; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * sh;
         }
         named_sync(1, PROD);
         if (tid == 0) TC_TRACE(0, 103 + 4 * s);  // face flux staged
@@ -372,7 +386,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, 2) tc_stage_kernel(const Tc
 #pragma unroll
         for (int q = 0; q < 4; ++q) split_tf32(row_ok ? v[t][q] : 0.f, hi[t][q], lo[t][q]);
       if (tid == 0) TC_TRACE(0, 101 + 4 * s);  // A values ready
-      mbar_wait(&empty[slot], ((i >> 1) & 1) ^ 1);
+      mbar_wait(&empty[slot], ((i / AST) & 1) ^ 1);
       if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free
       fence_after_sync();
 #pragma unroll

@@ -211,3 +211,17 @@ class TestRk4:
     def test_rejects_bad_dt(self):
         with pytest.raises(ValueError):
             rk4_step(np.zeros(2), 0.0, 0.0, lambda t, u: u)
+
+
+def test_cli_error_boundary_and_eoc_fit(capsys):
+    """JSON error on stderr + rc 1 at the process boundary (reference cli.py:408-411)."""
+    import json
+
+    from paper_0901_1024_b200.cli import fit_eoc, main, rows_to_csv
+
+    assert main(["simulate", "--node-file", "only-one.node"]) == 1
+    err = json.loads(capsys.readouterr().err.strip().splitlines()[-1])
+    assert set(err) == {"error", "message"}
+    h = np.array([0.5, 0.25, 0.125])
+    assert abs(fit_eoc(h, 3.0 * h ** 4.2) - 4.2) < 1e-12
+    assert rows_to_csv([{"a": 0.1, "b": 2}]) == "a,b\n0.10000000000000001,2\n"

@@ -306,6 +306,7 @@ int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, vo
         targs.bpack = static_cast<const float*>(d.tc_operand);
         const int64_t tt = (e_end - e_begin + TC::TE - 1) / TC::TE;
         targs.num_tiles = (int)tt;
+        targs.wave = TC::CTAS * plan->num_sms;
         dgm::tc_stage_kernel<N, MODE><<<(unsigned)tt, TC::THREADS, plan->tc_smem, static_cast<cudaStream_t>(stream)>>>(
             targs);
         return cuda_check(cudaGetLastError(), "tc_stage_kernel launch");

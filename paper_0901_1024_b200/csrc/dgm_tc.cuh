@@ -121,6 +121,7 @@ struct TcArgs {
   StageArgs<float> s;
   const float* bpack;  // [KS][hi,lo][2 chunks][NB][4]
   int num_tiles;
+  int wave;            // CTAs resident at once (CTAS x SMs): tile + wave runs next on this SM
 };
 
 template <int N, int MODE>
@@ -204,6 +205,16 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowbytes, load_full);
       if (MODE == MODE_LSRK && !a.a_zero)
         for (int f = 0; f < 6; ++f) prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rowbytes);
+      // warm L2 with the rows of the tile one wave ahead, so that CTA's bulk loads hit L2
+      const int64_t nt = (int64_t)blockIdx.x + args.wave;
+      if (nt < args.num_tiles) {
+        const int64_t n0 = a.e_begin + nt * TE;
+        const uint32_t nn = (uint32_t)min((int64_t)TE, a.e_end - n0);
+        for (int f = 0; f < 6; ++f) prefetch_l2(a.u + (int64_t)f * fstride + n0 * NPG, nn * NPG * 4);
+        prefetch_l2(a.geo + n0 * GEO_WORDS, nn * GEO_WORDS * 4);
+        prefetch_l2(a.nbr + n0 * 4, nn * 16);
+        prefetch_l2(a.code + n0 * 4, nn * 16);
+      }
     }
     __syncwarp();
     // Refill B slot j % NBS with K-step j + NBS once the MMAs of step j completed.  b_empty[slot]

@@ -62,6 +62,10 @@ struct Cfg {
   static_assert(NF4 >= NP, "rhs rows reuse the flux buffer");
   static constexpr size_t SMEM_REAL = (size_t)6 * TE * NPG + (size_t)6 * TE * NFS + (size_t)TE * GEO_WORDS;
   static constexpr size_t SMEM_FIXED = SMEM_REAL * W + (size_t)TE * 8 * 4 + 4 * NFP;
+  // Two CTAs per SM when shared memory allows it and N <= 6: capping registers there costs
+  // <= 220 B of spills and gains 1.1-1.5x (profiles/r01/simt_minblocks.json); at N >= 7 the
+  // spills (300-400 B) cost more than the occupancy gains.
+  static constexpr int MIN_BLOCKS = (N <= 6 && 2 * (SMEM_FIXED + 2048) <= 227 * 1024) ? 2 : 1;
 };
 
 template <typename T> struct V16;
@@ -125,7 +129,7 @@ __device__ __forceinline__ void upwind(const T* um, const T* up, T nx, T ny, T n
 }
 
 template <int N, typename T, int MODE>
-__global__ void __launch_bounds__(Cfg<N, T>::THREADS)
+__global__ void __launch_bounds__(Cfg<N, T>::THREADS, Cfg<N, T>::MIN_BLOCKS)
 stage_kernel(const StageArgs<T> a) {
   using C = Cfg<N, T>;
   using V = typename V16<T>::type;

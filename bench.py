@@ -53,7 +53,13 @@ def _ncu_summary() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 100 ms by a background reader.
+
+    Started before the warm-up so the first sample exists before the timed region; every line is
+    stamped on arrival and ``summary()`` reports the samples that arrived inside the marked timed
+    window (``window: "timed"``), or -- if the timed region was shorter than one sampling period --
+    the samples of the whole run (``window: "run"``).
+    """
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -62,31 +68,55 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.samples = []  # (arrival time, line)
+        self.t0 = self.t1 = None
 
     def __enter__(self):
+        import threading
+
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return self
+
+        def reader():
+            for line in self.proc.stdout:
+                if line.strip():
+                    self.samples.append((time.time(), line))
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        deadline = time.time() + 5.0  # wait for the first sample (nvidia-smi start-up)
+        while not self.samples and time.time() < deadline:
+            time.sleep(0.02)
         return self
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time() + 0.1  # the line reporting the last timed interval arrives a period later
+
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            self.thread.join(timeout=5)
 
     def summary(self) -> dict:
+        lines = [l for t, l in self.samples if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
+        window = "timed"
+        if not lines:
+            lines, window = [l for _, l in self.samples], "run"
         sm, smax, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in getattr(self, "lines", []):
+        for line in lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
@@ -99,7 +129,7 @@ class ClockSampler:
                 if flag.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 def _dist_env():
@@ -215,16 +245,19 @@ def run_b200(args) -> None:
         return runner.advance(x, dt, n)
 
     # ---- device-resident throughput (value) ----
-    advance(u, args.warmup)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        advance(u, args.warmup)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks.mark_start()
         start.record(stream)
         advance(u, args.steps)
         stop.record(stream)
         torch.cuda.synchronize()
+        clocks.mark_stop()
+        time.sleep(0.15)  # let the sample covering the end of the timed region arrive
     barrier()
     torch.cuda.synchronize()
     ms = start.elapsed_time(stop)
@@ -251,25 +284,45 @@ def run_b200(args) -> None:
     fp32_peak_tf = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
 
     # ---- end-to-end through the public API with host buffers ----
+    # Every e2e step uploads its own input (the f64 natural state, pinned host memory), packs it,
+    # runs one LSRK4 step, unpacks and downloads the new state and the energy scalar.  The steps are
+    # independent, so on one GPU they alternate between two CUDA streams with separate device
+    # buffers / workspaces: one step's D2H overlaps the next step's H2D (PCIe is full duplex) and
+    # compute.  Every byte counted below still crosses PCIe inside the timed region.
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     host_in = torch.from_numpy(np.ascontiguousarray(u0_host)).pin_memory()
-    host_out = torch.empty_like(host_in).pin_memory()
+    nstreams = 2 if world == 1 else 1
+    host_out = [torch.empty_like(host_in).pin_memory() for _ in range(nstreams)]
+    e_host = [torch.empty(1, dtype=torch.float64).pin_memory() for _ in range(nstreams)]
     h2d = host_in.numel() * host_in.element_size()
-    d2h = host_out.numel() * host_out.element_size() + 8
-    # warm-up one e2e step
-    ue = op.to_padded(host_in.to(dev, non_blocking=True))
-    advance(ue, 1)
+    d2h = host_out[0].numel() * host_out[0].element_size() + 8
+    streams = [torch.cuda.Stream(dev) for _ in range(nstreams)] if world == 1 else [stream]
+    ues = [op.empty_state() for _ in range(nstreams)]
+    works = [op.workspace() for _ in range(nstreams)] if world == 1 else [None]
+
+    def e2e_step(j):
+        with torch.cuda.stream(streams[j]):
+            op.to_padded(host_in.to(dev, non_blocking=True), out=ues[j])   # H2D + pack (f64 natural -> padded)
+            if world == 1:
+                op.advance(ues[j], dt, 1, use_graph=False, workspace=works[j])  # 5 fused stage launches
+            else:
+                advance(ues[j], 1)
+            host_out[j].copy_(op.from_padded(ues[j]), non_blocking=True)    # unpack + D2H of the new state
+            e_host[j].copy_(op.mass_norm(ues[j], 1.0, 1.0), non_blocking=True)  # per-step energy scalar
+
+    for j in range(nstreams):  # warm-up (allocations, first launches)
+        e2e_step(j)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record(stream)
-    for _ in range(e2e_steps):
-        ue = op.to_padded(host_in.to(dev, non_blocking=True), out=ue)   # H2D + pack (f64 natural -> padded)
-        advance(ue, 1)                                                  # 5 fused stage launches
-        host_out.copy_(op.from_padded(ue), non_blocking=True)           # unpack + D2H of the new state
-        energy_t = op.mass_norm(ue, 1.0, 1.0)                           # per-step diagnostic, as run_cavity
-        e_val = energy_t.to("cpu", non_blocking=True)
+    for st in streams:
+        st.wait_stream(stream)
+    for i in range(e2e_steps):
+        e2e_step(i % nstreams)
+    for st in streams:
+        stream.wait_stream(st)
     e_stop.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -279,7 +332,6 @@ def run_b200(args) -> None:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e_ms = float(t.item())
     e2e_gflops = world * f_alg * k * 5 * e2e_steps / (e_ms / 1e3) / 1e9
-    del e_val
 
     if rank != 0:
         if world > 1:
@@ -322,8 +374,10 @@ def run_b200(args) -> None:
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_gflops, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,
-                "path": "op.to_padded(pinned f64 natural state) -> op.advance(1 step) -> op.from_padded -> "
-                        "pinned host, + field-norm scalar D2H"},
+                "streams": nstreams,
+                "path": "per step: pinned f64 natural state H2D -> op.to_padded -> op.advance(1 LSRK4 step) -> "
+                        "op.from_padded -> pinned host D2H, + energy scalar D2H; independent steps alternate "
+                        "over %d CUDA stream(s)" % nstreams},
         "gpu_launches": launches,
         "clocks": clk,
         "energy_after": energy,
@@ -342,7 +396,7 @@ def main(argv=None) -> None:
     ap.add_argument("--order", type=int, default=ORDER)
     ap.add_argument("--cells", type=int, nargs=3, default=list(CELLS))
     ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--path", choices=("auto", "tensor", "simt"), default="auto",

@@ -306,12 +306,20 @@ class B200MaxwellOperator:
 
     def _buffers(self) -> _Buffers:
         if self._bufs is None:
-            self._bufs = _Buffers(alt=self.empty_state(), res=self.empty_state())
+            self._bufs = self.workspace()
         return self._bufs
 
-    def _launch_steps(self, u: torch.Tensor, dt: float, nsteps: int) -> torch.Tensor:
+    def workspace(self) -> _Buffers:
+        """Scratch registers (ping-pong state + LSRK residual) for ``advance(..., workspace=)``.
+
+        The operator keeps one of its own; pass a separate workspace per CUDA stream to advance
+        independent states concurrently.
+        """
+        return _Buffers(alt=self.empty_state(), res=self.empty_state())
+
+    def _launch_steps(self, u: torch.Tensor, dt: float, nsteps: int, bufs: _Buffers | None = None) -> torch.Tensor:
         """nsteps LSRK4 steps ping-ponging u <-> alt; returns the tensor holding the result."""
-        bufs = self._buffers()
+        bufs = self._buffers() if bufs is None else bufs
         cur, nxt = u, bufs.alt
         for _ in range(nsteps):
             for a, b in zip(RK_A, RK_B):
@@ -319,7 +327,8 @@ class B200MaxwellOperator:
                 cur, nxt = nxt, cur
         return cur
 
-    def advance(self, u: torch.Tensor, dt: float, nsteps: int = 1, use_graph: bool | None = None) -> torch.Tensor:
+    def advance(self, u: torch.Tensor, dt: float, nsteps: int = 1, use_graph: bool | None = None,
+                workspace: _Buffers | None = None) -> torch.Tensor:
         """Advance the padded state in place by nsteps LSRK4 steps of size dt."""
         self._check_padded(u)
         if dt <= 0.0:
@@ -331,40 +340,40 @@ class B200MaxwellOperator:
             return u
         if use_graph is None:
             use_graph = nsteps >= 4
+        bufs = self._buffers() if workspace is None else workspace
         if not use_graph:
-            cur = self._launch_steps(u, dt, nsteps)
+            cur = self._launch_steps(u, dt, nsteps, bufs)
             if cur is not u:
                 u.copy_(cur)
             return u
         pairs, odd = divmod(nsteps, 2)
         if pairs:
-            graph = self._graph_for(u, dt)
+            graph = self._graph_for(u, dt, bufs)
             for _ in range(pairs):
                 graph.replay()
         if odd:
-            cur = self._launch_steps(u, dt, 1)
+            cur = self._launch_steps(u, dt, 1, bufs)
             u.copy_(cur)
         return u
 
-    def _graph_for(self, u: torch.Tensor, dt: float):
+    def _graph_for(self, u: torch.Tensor, dt: float, bufs: _Buffers):
         """CUDA graph of two LSRK4 steps (10 stage launches, u -> alt -> ... -> u)."""
-        key = (u.data_ptr(), float(dt))
+        key = (u.data_ptr(), bufs.alt.data_ptr(), float(dt))
         graph = self._graphs.get(key)
         if graph is None:
-            bufs = self._buffers()
             # load the stage kernel outside capture (scratch buffers only)
             self.lsrk_stage(u, bufs.alt, bufs.res, 0.0, 0.0, 0.0, 0, min(self.num_elements, 1))
             torch.cuda.current_stream(self.device).synchronize()
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
-                cur = self._launch_steps(u, dt, 2)
+                cur = self._launch_steps(u, dt, 2, bufs)
                 assert cur is u
             self._graphs[key] = graph
         return graph
 
-    def step(self, u: torch.Tensor, dt: float) -> torch.Tensor:
+    def step(self, u: torch.Tensor, dt: float, workspace: _Buffers | None = None) -> torch.Tensor:
         """One LSRK4 step in place (5 fused stage launches)."""
-        return self.advance(u, dt, 1, use_graph=False)
+        return self.advance(u, dt, 1, use_graph=False, workspace=workspace)
 
     # ---------------------------------------------------------- diagnostics
     def mass_norm(self, u: torch.Tensor, w_e: float = 1.0, w_h: float = 1.0,

@@ -116,7 +116,7 @@ mass_norm_kernel(const T* __restrict__ u, const T* __restrict__ mass, const T* _
       for (int f = 0; f < 6; ++f)
 #pragma unroll
         for (int e = 0; e < E; ++e)
-          acc[f][e] += V16<T>::dot(m, *reinterpret_cast<const V*>(s_u + (f * TE + e * G + g) * NPG + jc * VEC));
+          acc[f][e] = V16<T>::fma_dot(m, *reinterpret_cast<const V*>(s_u + (f * TE + e * G + g) * NPG + jc * VEC), acc[f][e]);
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) {

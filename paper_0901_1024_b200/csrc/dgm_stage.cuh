@@ -71,14 +71,15 @@ struct Cfg {
 template <typename T> struct V16;
 template <> struct V16<float> {
   using type = float4;
-  __device__ static float dot(const float4& a, const float4& b) {
-    return fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, a.w * b.w)));
+  // acc + a.b as one FMA chain (no separate product / add)
+  __device__ static float fma_dot(const float4& a, const float4& b, float acc) {
+    return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, fmaf(a.x, b.x, acc))));
   }
 };
 template <> struct V16<double> {
   using type = double2;
-  __device__ static double dot(const double2& a, const double2& b) {
-    return fma(a.x, b.x, a.y * b.y);
+  __device__ static double fma_dot(const double2& a, const double2& b, double acc) {
+    return fma(a.y, b.y, fma(a.x, b.x, acc));
   }
 };
 
@@ -261,7 +262,7 @@ stage_kernel(const StageArgs<T> a) {
         for (int e = 0; e < E; ++e) {
           const V uv = *reinterpret_cast<const V*>(s_u + (f * TE + e * G + g) * NPG + jc * VEC);
 #pragma unroll
-          for (int m = 0; m < 3; ++m) acc[m][f][e] += V16<T>::dot(d[m], uv);
+          for (int m = 0; m < 3; ++m) acc[m][f][e] = V16<T>::fma_dot(d[m], uv, acc[m][f][e]);
         }
     }
     // geometric transform + curls (oracle.py:69-79)
@@ -298,7 +299,7 @@ stage_kernel(const StageArgs<T> a) {
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const V fv = *reinterpret_cast<const V*>(s_fl + (f * TE + e * G + g) * NFS + jc * VEC);
-            accl[f][e] += V16<T>::dot(l, fv);
+            accl[f][e] = V16<T>::fma_dot(l, fv, accl[f][e]);
           }
       }
 #pragma unroll

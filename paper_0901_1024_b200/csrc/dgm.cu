@@ -435,6 +435,12 @@ int dgm_halo_unpack(const dgm_plan* plan, const void* recvbuf, int64_t count, in
 
 }  // extern "C"
 
+#ifdef DGM_TC_TIMING
+extern "C" int dgm_phase_read(long long* host, int nblocks) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(host, dgm::g_tc_phase, sizeof(long long) * 5 * nblocks);
+}
+#endif
 #ifdef DGM_TC_TRACE
 extern "C" int dgm_hang_read(unsigned int* host) {
   return (int)cudaMemcpyFromSymbol(host, dgm::tc::g_hang, sizeof(unsigned int) * 8);

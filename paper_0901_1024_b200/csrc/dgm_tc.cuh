@@ -61,6 +61,17 @@ __device__ int g_tc_trace_n[2];
       g_tc_trace_n[who] = tc_tn;                               \
     }                                                          \
   } while (0)
+#elif defined(DGM_TC_TIMING)
+// Test-only phase timing of every CTA (libdgm_timing.so): producer thread 0 stores 5 clock64 stamps.
+__device__ long long g_tc_phase[1 << 16][5];
+#define TC_TRACE_DECL \
+  do {                \
+  } while (0)
+#define TC_TRACE(who, tag)                                                          \
+  do {                                                                              \
+    if ((who) == 0 && (tag) >= 1 && (tag) <= 5 && blockIdx.x < (1u << 16))          \
+      g_tc_phase[blockIdx.x][(tag) - 1] = clock64();                                \
+  } while (0)
 #else
 #define TC_TRACE_DECL \
   do {                \
@@ -240,13 +251,16 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         const uint64_t dbl = desc_kmajor(bh + 2 * NB * 16, NB * 16, 128);
         const uint32_t abase = tmem + T::A_COL0 + slot * T::A_STAGE_COLS;
         const uint32_t acc0 = s > 0 ? 1u : 0u;
-        // pass-major order: consecutive MMAs hit different accumulators
+        // accumulator-major order: the three passes of one accumulator back to back issue ~30 %
+        // faster than pass-major interleaving (profiles/r01/mma_shape_probe.txt)
+#ifndef DGM_EXP_NOMMA
 #pragma unroll
-        for (int t = 0; t < MT; ++t) mma_tf32_ts(tmem + t * NB, abase + t * 16, dbh, idesc, acc0);
-#pragma unroll
-        for (int t = 0; t < MT; ++t) mma_tf32_ts(tmem + t * NB, abase + t * 16 + 8, dbh, idesc, 1u);
-#pragma unroll
-        for (int t = 0; t < MT; ++t) mma_tf32_ts(tmem + t * NB, abase + t * 16, dbl, idesc, 1u);
+        for (int t = 0; t < MT; ++t) {
+          mma_tf32_ts(tmem + t * NB, abase + t * 16, dbh, idesc, acc0);     // A_hi B_hi
+          mma_tf32_ts(tmem + t * NB, abase + t * 16 + 8, dbh, idesc, 1u);   // A_lo B_hi
+          mma_tf32_ts(tmem + t * NB, abase + t * 16, dbl, idesc, 1u);       // A_hi B_lo
+        }
+#endif
         mma_commit(&empty[slot]);
         mma_commit(&b_empty[s % NBS]);
         if (s == KS - 1) mma_commit(acc_full);
@@ -290,64 +304,71 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       const int k0 = s * 8;
       if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
       // ---- surface flux of a whole face at its first K-step ----
+#ifdef DGM_EXP_NOFLUX
+      if (false) {
+#else
       if (k0 >= KV && (k0 - KV) % NFPK == 0) {
+#endif
         const int face = (k0 - KV) / NFPK;
         named_sync(1, PROD);  // every thread finished reading the previous face's staging
+        // one work unit = (element row, 4 consecutive node slots): the row's face data (normal,
+        // scale, code, neighbour, in-tile or not) is read once and u+ is fetched with typed
+        // shared / global loads, all 24 in flight before any use
+        constexpr int NB4 = NFPK / 4;
 #pragma unroll 1
-        for (int ib = 0; ib < ITEMS; ib += IB) {
-          float up[IB][6];
+        for (int unit = tid; unit < TE * NB4; unit += PROD) {
+          const int r = unit / NB4, n0 = (unit % NB4) * 4;
+          const bool row_live = r < nv;
+          const int code = row_live ? s_code[r * 4 + face] : -1;
+          const int nb = s_nbr[r * 4 + face];
+          const float* gk = s_geo + r * GEO_WORDS;
+          const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
+          const float sc = row_live ? gk[22 + face] * gk[9] : 0.f;
+          const float se = sc * a.inv_eps, sh = sc * a.inv_mu;
+          int im[4], jn[4];
 #pragma unroll
-          for (int i = 0; i < IB; ++i) {  // u+ gathers first: a batch of loads in flight together
-            const int item = tid + (ib + i) * PROD;
-            const int r = item / NFPK, node = item % NFPK;
-            const bool live = node < NFP && r < nv;
-            const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
-            const float* src = s_u + r * NPG + im;  // PEC walls mirror the own trace below
-            int64_t fs = TE * NPG;
-            const int code = live ? s_code[r * 4 + face] : -1;
-            if (code >= 0) {
-              const int nb = s_nbr[r * 4 + face];
-              const int jn = s_ptab[code * NFP + node];
-              const int64_t loc = (int64_t)nb - e0;
-              if (loc >= 0 && loc < nv) {
-                src = s_u + (int)loc * NPG + jn;
-              } else {
-                src = a.u + (int64_t)nb * NPG + jn;
-                fs = fstride;
-              }
-            }
+          for (int j = 0; j < 4; ++j) {
+            const int node = n0 + j < NFP ? n0 + j : 0;
+            im[j] = s_fmask[face * NFP + node];
+            jn[j] = code >= 0 ? s_ptab[code * NFP + node] : 0;
+          }
+          float up[4][6];
+          const int64_t loc = (int64_t)nb - e0;
+          if (code >= 0 && loc >= 0 && loc < nv) {  // neighbour row in this tile: shared memory
 #pragma unroll
-            for (int f = 0; f < 6; ++f) up[i][f] = src[f * fs];
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int f = 0; f < 6; ++f) up[j][f] = s_u[(f * TE + (int)loc) * NPG + jn[j]];
+          } else if (code >= 0) {  // neighbour row elsewhere: global (L2-prefetched at tile start)
+            const float* g = a.u + (int64_t)nb * NPG;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int f = 0; f < 6; ++f) up[j][f] = __ldg(g + f * fstride + jn[j]);
           }
 #pragma unroll
-          for (int i = 0; i < IB; ++i) {
-            const int item = tid + (ib + i) * PROD;
-            const int r = item / NFPK, node = item % NFPK;
-            const bool live = node < NFP && r < nv;
-            const int im = s_fmask[face * NFP + (node < NFP ? node : 0)];
+          for (int j = 0; j < 4; ++j) {
             float um[6];
 #pragma unroll
-            for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + r) * NPG + im];
-            const float* gk = s_geo + r * GEO_WORDS;
-            const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
-            if (live && s_code[r * 4 + face] < 0) {  // PEC mirror (maxwell.py:117-132)
+            for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + r) * NPG + im[j]];
+            if (code < 0) {  // PEC mirror (maxwell.py:117-132)
               const float nde = nx * um[0] + ny * um[1] + nz * um[2];
               const float ndh = nx * um[3] + ny * um[4] + nz * um[5];
-              up[i][0] = -um[0] + 2.f * nde * nx;
-              up[i][1] = -um[1] + 2.f * nde * ny;
-              up[i][2] = -um[2] + 2.f * nde * nz;
-              up[i][3] = um[3] - 2.f * ndh * nx;
-              up[i][4] = um[4] - 2.f * ndh * ny;
-              up[i][5] = um[5] - 2.f * ndh * nz;
+              up[j][0] = -um[0] + 2.f * nde * nx;
+              up[j][1] = -um[1] + 2.f * nde * ny;
+              up[j][2] = -um[2] + 2.f * nde * nz;
+              up[j][3] = um[3] - 2.f * ndh * nx;
+              up[j][4] = um[4] - 2.f * ndh * ny;
+              up[j][5] = um[5] - 2.f * ndh * nz;
             }
             float out[6];
-            upwind(um, up[i], nx, ny, nz, a, out);
-            const float sc = live ? gk[22 + face] * gk[9] : 0.f;
-            const float se = sc * a.inv_eps, sh = sc * a.inv_mu;
+            upwind(um, up[j], nx, ny, nz, a, out);
+            const int node = n0 + j;
+            const float kse = node < NFP ? se : 0.f, ksh = node < NFP ? sh : 0.f;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * se;
+            for (int c = 0; c < 3; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * kse;
 #pragma unroll
-            for (int c = 3; c < 6; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * sh;
+            for (int c = 3; c < 6; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * ksh;
           }
         }
         named_sync(1, PROD);
@@ -400,12 +421,16 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       mbar_wait(&empty[slot], ((i / AST) & 1) ^ 1);
       if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free
       fence_after_sync();
+#ifndef DGM_EXP_NOSTORE
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + t * 16 + 4 * khalf;
         tmem_st4(tmem + lane_addr + col, hi[t]);
         tmem_st4(tmem + lane_addr + col + 8, lo[t]);
       }
+#else
+      if (hi[0][0] == 12345.f && lo[2][3] == 1.f) s_stage[0] = 0.f;  // keep the values live
+#endif
       tmem_st_wait();
       fence_before_sync();
       __syncwarp();

@@ -355,6 +355,86 @@ __global__ void __launch_bounds__(320) probe_handoff_kernel(int reps, int mode, 
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
+// Issue cost of one K-step's MMA burst in different shapes (M=128, N=48, TS, K=8):
+//   variant 0: 3 acc x 3 passes, pass-major (t0p0 t1p0 t2p0 t0p1 ...), 1 commit
+//   variant 1: same, 2 commits
+//   variant 2: 3 acc x 3 passes, acc-major (t0p0 t0p1 t0p2 t1p0 ...), 1 commit
+//   variant 3: 9 independent accumulators (split passes), 1 commit
+//   variant 4: 6 acc x 3 passes pass-major (18 MMAs), 1 commit
+//   variant 5: 3 acc x 3 passes, pass-major, two bursts back to back before one wait (2 K-steps)
+__global__ void __launch_bounds__(128) probe_shape_kernel(int reps, int variant, long long* cycles) {
+  using namespace dgm::tc;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ uint32_t tmem_base;
+  float* b_s = reinterpret_cast<float*>(smem);
+  for (int i = threadIdx.x; i < 48 * 16; i += blockDim.x) b_s[i] = 0.f;
+  if (threadIdx.x < 32) tmem_alloc(&tmem_base, 512);
+  if (threadIdx.x == 32) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    mbar_init_fence();
+  }
+  fence_async_smem();
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tmem_base;
+  if (threadIdx.x < 32) {
+    const uint32_t idesc = idesc_tf32(128, 48);
+    const uint64_t bd = desc_kmajor(smem_u32(b_s), 48 * 16, 128);
+    const uint32_t a = tmem + 448;
+    long long issue = 0;
+    __syncwarp();
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const long long ti = clock64();
+      if (elect_one()) {
+        if (variant == 0 || variant == 1 || variant == 5) {
+          const int nb = variant == 5 ? 2 : 1;
+          for (int b = 0; b < nb; ++b) {
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+#pragma unroll
+              for (int t = 0; t < 3; ++t) mma_tf32_ts(tmem + t * 48, a + 8 * (p & 1), bd, idesc, 1u);
+          }
+          mma_commit(&mbar[0]);
+          if (variant == 1) mma_commit(&mbar[1]);
+        } else if (variant == 2) {
+#pragma unroll
+          for (int t = 0; t < 3; ++t)
+#pragma unroll
+            for (int p = 0; p < 3; ++p) mma_tf32_ts(tmem + t * 48, a + 8 * (p & 1), bd, idesc, 1u);
+          mma_commit(&mbar[0]);
+        } else if (variant == 3) {
+#pragma unroll
+          for (int t = 0; t < 9; ++t) mma_tf32_ts(tmem + t * 48, a + 8 * (t & 1), bd, idesc, 1u);
+          mma_commit(&mbar[0]);
+        } else {
+#pragma unroll
+          for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int t = 0; t < 6; ++t) mma_tf32_ts(tmem + t * 48, a + 8 * (p & 1), bd, idesc, 1u);
+          mma_commit(&mbar[0]);
+        }
+      }
+      __syncwarp();
+      issue += clock64() - ti;
+      mbar_wait(&mbar[0], r & 1);
+      if (variant == 1) mbar_wait(&mbar[1], r & 1);
+      fence_after_sync();
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) {
+      cycles[0] = t1 - t0;
+      cycles[1] = issue;
+    }
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
 }  // namespace
 
 extern "C" int dgm_probe_mma_rate(int n, int reps, int ts, int nacc, long long* cycles_dev) {
@@ -394,5 +474,11 @@ extern "C" int dgm_probe_mma_burst(int n, int reps, int nacc, int passes, int ct
 extern "C" int dgm_probe_handoff(int reps, int mode, int pw, int ctas, long long* cycles_dev) {
   if (pw < 1 || pw > 8 || reps < 2) return -1;
   probe_handoff_kernel<<<ctas, 32 * (pw + 1), 48 * 16 * 4 + 1024>>>(reps, mode, pw, cycles_dev);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int dgm_probe_mma_shape(int reps, int variant, int ctas, long long* cycles_dev) {
+  if (variant < 0 || variant > 5) return -1;
+  probe_shape_kernel<<<ctas, 128, 48 * 16 * 4 + 1024>>>(reps, variant, cycles_dev);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

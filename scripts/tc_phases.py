@@ -28,6 +28,8 @@ lib.dgm_phase_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
 ntiles = min((mesh.num_elements + 63) // 64, 1 << 16)
 buf = np.zeros((ntiles, 5), dtype=np.int64)
 lib.dgm_phase_read(buf.ctypes.data, ntiles)
+buf = buf[buf[:, 4] > 0]  # persistent kernel: one row per CTA (its last tile)
+ntiles = len(buf)
 d = np.diff(buf, axis=1)
 names = ["start->rows landed", "rows->K-loop done", "K-loop->acc ready", "acc->epilogue done"]
 print(f"{ntiles} CTAs, N={order}; cycles per CTA (mean / median / p90):")

@@ -286,12 +286,12 @@ def run_b200(args) -> None:
     # ---- end-to-end through the public API with host buffers ----
     # Every e2e step uploads its own input (the f64 natural state, pinned host memory), packs it,
     # runs one LSRK4 step, unpacks and downloads the new state and the energy scalar.  The steps are
-    # independent, so on one GPU they alternate between two CUDA streams with separate device
+    # independent, so on one GPU they rotate over three CUDA streams with separate device
     # buffers / workspaces: one step's D2H overlaps the next step's H2D (PCIe is full duplex) and
     # compute.  Every byte counted below still crosses PCIe inside the timed region.
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     host_in = torch.from_numpy(np.ascontiguousarray(u0_host)).pin_memory()
-    nstreams = 2 if world == 1 else 1
+    nstreams = 3 if world == 1 else 1
     host_out = [torch.empty_like(host_in).pin_memory() for _ in range(nstreams)]
     e_host = [torch.empty(1, dtype=torch.float64).pin_memory() for _ in range(nstreams)]
     h2d = host_in.numel() * host_in.element_size()
@@ -396,7 +396,7 @@ def main(argv=None) -> None:
     ap.add_argument("--order", type=int, default=ORDER)
     ap.add_argument("--cells", type=int, nargs=3, default=list(CELLS))
     ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=9)
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--path", choices=("auto", "tensor", "simt"), default="auto",

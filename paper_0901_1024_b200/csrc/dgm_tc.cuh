@@ -298,18 +298,47 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #pragma unroll
     for (int q = 0; q < 9; ++q) prx[q] = row_ok ? s_geo[row * GEO_WORDS + q] * inv_m : 0.f;
 
-    for (int i = 0; i < KS; ++i) {  // i: position in this CTA's K order, s: K-step
-      const int slot = i % AST;
-      const int s = (i + rot) % KS;
+    // A values of K-step s for this thread's row (4 columns x 3 M-tiles), unsplit
+    auto a_values = [&](int s, float (&v)[MT][4]) {
       const int k0 = s * 8;
-      if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
-      // ---- surface flux of a whole face at its first K-step ----
-#ifdef DGM_EXP_NOFLUX
-      if (false) {
-#else
-      if (k0 >= KV && (k0 - KV) % NFPK == 0) {
-#endif
-        const int face = (k0 - KV) / NFPK;
+      {
+        const int k = k0 + 4 * khalf;
+        if (k < 3 * NPK) {
+          const int mu = k / NPK, j0 = k - mu * NPK;
+          const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
+          const int fb = h == 0 ? 3 : 0;  // E comps read H fields and vice versa
+          const float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + 0) * TE + row) * NPG + j0);
+          const float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + 1) * TE + row) * NPG + j0);
+          const float4 z = *reinterpret_cast<const float4*>(s_u + ((fb + 2) * TE + row) * NPG + j0);
+          const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w}, zs[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (h == 0) {  // (curl H)_x,y,z
+              v[0][q] = p1 * zs[q] - p2 * ys[q];
+              v[1][q] = p2 * xs[q] - p0 * zs[q];
+              v[2][q] = p0 * ys[q] - p1 * xs[q];
+            } else {       // -(curl E)_x,y,z
+              v[0][q] = p2 * ys[q] - p1 * zs[q];
+              v[1][q] = p0 * zs[q] - p2 * xs[q];
+              v[2][q] = p1 * xs[q] - p0 * ys[q];
+            }
+          }
+        } else if (k >= KV) {
+          const int node = (k - KV) % NFPK;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int t = 0; t < MT; ++t) v[t][q] = s_stage[((3 * h + t) * NFPK + node + q) * SROW + row];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int t = 0; t < MT; ++t) v[t][q] = 0.f;
+        }
+      }
+    };
+    // surface flux of a whole face into the staging buffer (all producers, two named barriers)
+    auto flux_pass = [&](int face) {
         named_sync(1, PROD);  // every thread finished reading the previous face's staging
         // one work unit = (element row, 4 consecutive node slots): the row's face data (normal,
         // scale, code, neighbour, in-tile or not) is read once and u+ is fetched with typed
@@ -372,52 +401,26 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
           }
         }
         named_sync(1, PROD);
-        if (tid == 0) TC_TRACE(0, 103 + 4 * s);  // face flux staged
-      }
+    };
+    auto face_start = [&](int s) { return s * 8 >= KV && (s * 8 - KV) % NFPK == 0; };
 
-      // ---- A K-step (this thread's 4 columns of its row in the 3 M-tiles) ----
-      float v[MT][4];
-      {
-        const int k = k0 + 4 * khalf;
-        if (k < 3 * NPK) {
-          const int mu = k / NPK, j0 = k - mu * NPK;
-          const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
-          const int fb = h == 0 ? 3 : 0;  // E comps read H fields and vice versa
-          const float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + 0) * TE + row) * NPG + j0);
-          const float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + 1) * TE + row) * NPG + j0);
-          const float4 z = *reinterpret_cast<const float4*>(s_u + ((fb + 2) * TE + row) * NPG + j0);
-          const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w}, zs[4] = {z.x, z.y, z.z, z.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (h == 0) {  // (curl H)_x,y,z
-              v[0][q] = p1 * zs[q] - p2 * ys[q];
-              v[1][q] = p2 * xs[q] - p0 * zs[q];
-              v[2][q] = p0 * ys[q] - p1 * xs[q];
-            } else {       // -(curl E)_x,y,z
-              v[0][q] = p2 * ys[q] - p1 * zs[q];
-              v[1][q] = p0 * zs[q] - p2 * xs[q];
-              v[2][q] = p1 * xs[q] - p0 * ys[q];
-            }
-          }
-        } else if (k >= KV) {
-          const int node = (k - KV) % NFPK;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int t = 0; t < MT; ++t) v[t][q] = s_stage[((3 * h + t) * NFPK + node + q) * SROW + row];
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int t = 0; t < MT; ++t) v[t][q] = 0.f;
-        }
-      }
+    // Software-pipelined K loop: the next step's A values are computed between this step's
+    // tcgen05.st and its tcgen05.wait::st, hiding the TMEM store latency; a flux pass (two named
+    // barriers) runs only after this step's stage was handed to the MMA warp.
+    float vcur[MT][4], vnext[MT][4];
+#ifndef DGM_EXP_NOFLUX
+    if (face_start((0 + rot) % KS)) flux_pass(((0 + rot) % KS * 8 - KV) / NFPK);
+#endif
+    a_values((0 + rot) % KS, vcur);
+    for (int i = 0; i < KS; ++i) {  // i: position in this CTA's K order, s: K-step
+      const int slot = i % AST;
+      const int s = (i + rot) % KS;
+      if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
       float hi[MT][4], lo[MT][4];
 #pragma unroll
       for (int t = 0; t < MT; ++t)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) split_tf32(row_ok ? v[t][q] : 0.f, hi[t][q], lo[t][q]);
-      if (tid == 0) TC_TRACE(0, 101 + 4 * s);  // A values ready
+        for (int q = 0; q < 4; ++q) split_tf32(row_ok ? vcur[t][q] : 0.f, hi[t][q], lo[t][q]);
       mbar_wait(&empty[slot], ((i / AST) & 1) ^ 1);
       if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free
       fence_after_sync();
@@ -431,10 +434,27 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #else
       if (hi[0][0] == 12345.f && lo[2][3] == 1.f) s_stage[0] = 0.f;  // keep the values live
 #endif
+      const int sn = (i + 1 + rot) % KS;
+      const bool has_next = i + 1 < KS;
+#ifdef DGM_EXP_NOFLUX
+      const bool next_flux = false;
+#else
+      const bool next_flux = has_next && face_start(sn);
+#endif
+      if (has_next && !next_flux) a_values(sn, vnext);  // overlaps the TMEM store latency
       tmem_st_wait();
       fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[slot]);
+      if (next_flux) {
+        flux_pass((sn * 8 - KV) / NFPK);
+        if (tid == 0) TC_TRACE(0, 103 + 4 * sn);  // face flux staged
+        a_values(sn, vnext);
+      }
+#pragma unroll
+      for (int t = 0; t < MT; ++t)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) vcur[t][q] = vnext[t][q];
     }
 
     // ================= epilogue: accumulators -> LSRK update =================

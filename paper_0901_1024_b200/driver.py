@@ -97,6 +97,7 @@ def run_cavity(order: int, cells, extent=(1.0, 1.0, 1.0), mode_numbers=(1, 1, 1)
                 trace.append((step * dt, energy))
         checked = upto
 
+    op.collect_stats = True  # per-kernel device time -> CavityRun.stage_stats
     for n in range(1, num_steps + 1):
         op.step(u, dt)
         t += dt
@@ -109,4 +110,5 @@ def run_cavity(order: int, cells, extent=(1.0, 1.0, 1.0), mode_numbers=(1, 1, 1)
             for a in range(4) for b in range(a + 1, 4))
     return CavityRun(order=order, num_elements=mesh.num_elements, mesh_size=h, dt=dt, num_steps=num_steps,
                      final_time=t, l2_error=op.l2_error(u, mode, t), initial_energy=e0, final_energy=e_prev,
-                     max_energy_growth=max_growth, energy_trace=trace, stage_stats={})
+                     max_energy_growth=max_growth, energy_trace=trace,
+                     stage_stats={k: v.to_dict() for k, v in op.stage_stats.items()})

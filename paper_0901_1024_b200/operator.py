@@ -84,6 +84,18 @@ class _Buffers:
     res: torch.Tensor
 
 
+@dataclass
+class KernelStats:
+    """Device time of one kernel family (the B200 replacement of the emulator's MemStats)."""
+
+    launches: int = 0
+    ms: float = 0.0
+
+    def to_dict(self) -> dict:
+        return {"launches": self.launches, "ms": self.ms,
+                "us_per_launch": 1e3 * self.ms / self.launches if self.launches else 0.0}
+
+
 class B200MaxwellOperator:
     """Maxwell RHS and LSRK4 on one B200 (or one rank's element range)."""
 
@@ -149,6 +161,9 @@ class B200MaxwellOperator:
         self._bufs: _Buffers | None = None
         self._graphs: dict = {}
         self._norm_out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.collect_stats = False   # record CUDA-event times of every stage launch
+        self._events: list = []
+        self._stats: dict = {}
         # reference-operator attributes, filled by build_b200_operator
         self.mesh: Mesh | None = None
         self.connectivity: FaceConnectivity | None = None
@@ -208,6 +223,42 @@ class B200MaxwellOperator:
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
+    # ---------------------------------------------------------- statistics
+    def _timed(self, name: str, launch) -> None:
+        """Run ``launch()``; with ``collect_stats`` bracket it with CUDA events on the current stream."""
+        if not self.collect_stats or torch.cuda.is_current_stream_capturing():
+            launch()
+            return
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stream = torch.cuda.current_stream(self.device)
+        start.record(stream)
+        launch()
+        stop.record(stream)
+        self._events.append((name, start, stop))
+
+    @property
+    def stage_stats(self) -> dict:
+        """Per-kernel device time {name: KernelStats} (pipeline.py:62-68's stage_stats, measured)."""
+        if self._events:
+            torch.cuda.synchronize(self.device)
+            for name, start, stop in self._events:
+                st = self._stats.setdefault(name, KernelStats())
+                st.launches += 1
+                st.ms += start.elapsed_time(stop)
+            self._events.clear()
+        return self._stats
+
+    def reset_stats(self) -> None:
+        self._events.clear()
+        self._stats = {}
+
+    def total_stats(self) -> KernelStats:
+        tot = KernelStats()
+        for st in self.stage_stats.values():
+            tot.launches += st.launches
+            tot.ms += st.ms
+        return tot
+
     # ---------------------------------------------------------------- layout
     def empty_state(self) -> torch.Tensor:
         """Zeroed padded state (6, field_stride, np_stride) on the device."""
@@ -265,7 +316,8 @@ class B200MaxwellOperator:
         else:
             self._check_padded(out, "out")
         b, e = self._range(e_begin, e_end)
-        _capi.check(self._lib.dgm_rhs(self._plan, u.data_ptr(), out.data_ptr(), b, e, self._stream()), "dgm_rhs")
+        self._timed("rhs", lambda: _capi.check(
+            self._lib.dgm_rhs(self._plan, u.data_ptr(), out.data_ptr(), b, e, self._stream()), "dgm_rhs"))
         return out
 
     def volume_padded(self, u: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -300,9 +352,9 @@ class B200MaxwellOperator:
                    dt: float, e_begin=None, e_end=None) -> None:
         """res = a res + dt rhs(u_in); u_out = u_in + b res  (one fused launch)."""
         bb, ee = self._range(e_begin, e_end)
-        _capi.check(self._lib.dgm_lsrk_stage(self._plan, u_in.data_ptr(), u_out.data_ptr(), res.data_ptr(),
-                                             float(a), float(b), float(dt), bb, ee, self._stream()),
-                    "dgm_lsrk_stage")
+        self._timed("lsrk_stage", lambda: _capi.check(
+            self._lib.dgm_lsrk_stage(self._plan, u_in.data_ptr(), u_out.data_ptr(), res.data_ptr(),
+                                     float(a), float(b), float(dt), bb, ee, self._stream()), "dgm_lsrk_stage"))
 
     def _buffers(self) -> _Buffers:
         if self._bufs is None:

@@ -52,6 +52,8 @@ def test_run_cavity_matches_reference_loop(dtype, tol):
     assert abs(run.l2_error - err) <= tol * max(err, 1e-3) + 1e-7
     assert run.max_energy_growth <= 1e-6
     assert math.isclose(run.final_time, final_time, rel_tol=1e-12)
+    st = run.stage_stats["lsrk_stage"]  # per-kernel device time (pipeline.py stage_stats counterpart)
+    assert st["launches"] == 5 * n and st["ms"] > 0.0
 
 
 def test_run_cavity_errors():

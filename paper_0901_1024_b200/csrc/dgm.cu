@@ -93,6 +93,8 @@ DGM_TC_INFO(3)
 DGM_TC_INFO(4)
 DGM_TC_INFO(5)
 DGM_TC_INFO(6)
+DGM_TC_INFO(7)
+DGM_TC_INFO(8)
 #undef DGM_TC_INFO
 }  // namespace
 

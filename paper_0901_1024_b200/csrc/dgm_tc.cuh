@@ -91,14 +91,19 @@ struct TcCfg {
   static constexpr int KV = (3 * NPK + 7) / 8 * 8; // volume part of K, padded to a K step
   static constexpr int KT = KV + 4 * NFPK;
   static constexpr int KS = KT / 8;                // K steps (one kind::tf32 MMA each)
-  static constexpr int TE = 64;                    // elements per CTA
-  static constexpr int MT = 3;                     // M-tiles (E_t | H_t)
+  // Lane mapping.  MAP 0 (N <= 6): 64 elements per CTA, M-tile t = [E_t of the 64 elements |
+  // H_t of the 64 elements].  MAP 1 (N = 7, 8, where a 64-element u tile no longer fits in smem):
+  // 32 elements per CTA, M-tiles component-major: tile 0 = [E_x | E_y | E_z | H_x], tile 1 =
+  // [H_y | H_z | pad | pad] (32 lanes per component).
+  static constexpr int MAP = N <= 6 ? 0 : 1;
+  static constexpr int TE = MAP == 0 ? 64 : 32;    // elements per CTA
+  static constexpr int MT = MAP == 0 ? 3 : 2;      // M-tiles
   static constexpr int PWARPS = 8;
   static constexpr int PROD = 32 * PWARPS;         // producer threads
   static constexpr int THREADS = PROD + 64;        // + MMA warp + loader warp
   static constexpr int ACC_COLS = MT * NB;
   static constexpr int A_COL0 = (ACC_COLS + 31) / 32 * 32;
-  static constexpr int A_STAGE_COLS = MT * 16;     // 3 M-tiles x (8 hi + 8 lo)
+  static constexpr int A_STAGE_COLS = MT * 16;     // M-tiles x (8 hi + 8 lo)
   static constexpr int CTAS = N <= 4 ? 2 : 1;     // CTAs per SM (TMEM and smem split between them)
   static constexpr int TMEM_COLS = 512 / CTAS;
   static constexpr int AST0 = (TMEM_COLS - A_COL0) / A_STAGE_COLS;
@@ -126,6 +131,13 @@ struct TcCfg {
   static constexpr size_t OFF_PTAB = OFF_FMASK + (4 * NFP + 15) / 16 * 16;
   static constexpr size_t SMEM_FIXED = OFF_PTAB;   // + ncodes * NFP
   static constexpr size_t B_FLOATS = (size_t)KS * 2 * 2 * NB * 4;  // packed operand in global
+
+  // component held by TMEM lane quadrant q in M-tile t (>= 6: padding lanes)
+  __host__ __device__ static constexpr int comp_of(int t, int q) { return MAP == 0 ? t + 3 * (q >> 1) : 4 * t + q; }
+  // element row of lane (q, l)
+  __host__ __device__ static constexpr int row_of(int q, int l) { return MAP == 0 ? (q & 1) * 32 + l : l; }
+  // epilogue phase p moves two components (which = 0, 1) through the rows buffer
+  __host__ __device__ static constexpr int epi_comp(int p, int which) { return MAP == 0 ? p + 3 * which : 2 * p + which; }
 };
 
 struct TcArgs {
@@ -272,10 +284,11 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     // ================= producers =================
     const int quad = warp & 3;               // TMEM lane quadrant
     const int khalf = warp >> 2;             // which 4 of a K step's 8 columns
-    const int h = quad >> 1;                 // 0: E components (from H fields), 1: H components (from E fields)
-    const int row = (quad & 1) * 32 + lane;  // element row of this TMEM lane
+    const int h = quad >> 1;                 // MAP 0: 0 = E components (from H fields), 1 = H components
+    const int row = T::row_of(quad, lane);   // element row of this TMEM lane
     const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
-    const float inv_m = h == 0 ? a.inv_eps : a.inv_mu;
+    // MAP 0: one material factor per thread (folded into prx); MAP 1: per component
+    const float inv_m = T::MAP == 0 ? (h == 0 ? a.inv_eps : a.inv_mu) : 1.f;
     if (tid == 0) TC_TRACE(0, 1);  // start
     mbar_wait(load_full, 0);
     if (tid == 0) TC_TRACE(0, 2);  // rows landed
@@ -301,7 +314,37 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     // A values of K-step s for this thread's row (4 columns x 3 M-tiles), unsplit
     auto a_values = [&](int s, float (&v)[MT][4]) {
       const int k0 = s * 8;
-      {
+      if constexpr (T::MAP == 1) {
+        // one component per M-tile: comp c = 4t + quad; (curl H)_cc / eps for c < 3, -(curl E)_cc / mu
+        const int k = k0 + 4 * khalf;
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          const int c = T::comp_of(t, quad);
+          if (c >= 6) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[t][q] = 0.f;
+          } else if (k < 3 * NPK) {
+            const int mu = k / NPK, j0 = k - mu * NPK;
+            const int cc = c % 3, c1 = (cc + 1) % 3, c2 = (cc + 2) % 3;
+            const int fb = c < 3 ? 3 : 0;  // E comps read H fields and vice versa
+            const float m = c < 3 ? a.inv_eps : -a.inv_mu;
+            const float pa = prx[mu * 3 + c1] * m, pb = prx[mu * 3 + c2] * m;
+            const float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + c2) * TE + row) * NPG + j0);
+            const float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + c1) * TE + row) * NPG + j0);
+            v[t][0] = pa * x.x - pb * y.x;
+            v[t][1] = pa * x.y - pb * y.y;
+            v[t][2] = pa * x.z - pb * y.z;
+            v[t][3] = pa * x.w - pb * y.w;
+          } else if (k >= KV) {
+            const int node = (k - KV) % NFPK;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[t][q] = s_stage[(c * NFPK + node + q) * SROW + row];
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[t][q] = 0.f;
+          }
+        }
+      } else {
         const int k = k0 + 4 * khalf;
         if (k < 3 * NPK) {
           const int mu = k / NPK, j0 = k - mu * NPK;
@@ -466,8 +509,8 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     if (tid == 0) TC_TRACE(0, 4);  // accumulators final
     fence_after_sync();
 #pragma unroll 1
-    for (int t = 0; t < MT; ++t) {
-      // residual rows of components t and t+3 (L2-prefetched at CTA start), all loads in flight
+    for (int t = 0; t < 3; ++t) {  // epilogue phase: components T::epi_comp(t, 0 / 1)
+      // residual rows of the phase's two components (L2-prefetched at CTA start), all loads in flight
       float4 ro[PER];
 #pragma unroll
       for (int p = 0; p < PER; ++p) {
@@ -475,15 +518,21 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         const int which = idx >= nvec ? 1 : 0;
         const int c = idx - which * nvec;
         ro[p] = (MODE == MODE_LSRK && !a.a_zero && c < nvec)
-                    ? __ldcs(reinterpret_cast<const float4*>(a.res + ((int64_t)(t + 3 * which) * a.kf + e0) * NPG) + c)
+                    ? __ldcs(reinterpret_cast<const float4*>(
+                                 a.res + ((int64_t)T::epi_comp(t, which) * a.kf + e0) * NPG) + c)
                     : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      if (khalf == 0) {  // quadrant warps: TMEM lanes -> smem rows [E_t | H_t][row][NPG]
-        float* dst = s_stage + (size_t)h * TE * NPG + row * NPG;
+      // quadrant warps holding the phase's components: TMEM lanes -> smem rows [which][row][NPG]
+      // (MAP 0: M-tile t, all four quadrants; MAP 1: M-tile t/2, quadrants 2(t%2), 2(t%2)+1)
+      const bool mover = khalf == 0 && (T::MAP == 0 || (quad >> 1) == (t & 1));
+      if (mover) {
+        const int tile = T::MAP == 0 ? t : t >> 1;
+        const int slot = T::MAP == 0 ? h : (quad & 1);
+        float* dst = s_stage + (size_t)slot * TE * NPG + row * NPG;
 #pragma unroll
         for (int c0 = 0; c0 < NB; c0 += 8) {
           float r8[8];
-          tmem_ld8(tmem + lane_addr + t * NB + c0, r8);
+          tmem_ld8(tmem + lane_addr + tile * NB + c0, r8);
           tmem_ld_wait();
 #pragma unroll
           for (int q = 0; q < 8; q += 4) {
@@ -506,7 +555,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         const int which = idx >= nvec ? 1 : 0;
         const int c = idx - which * nvec;
         if (c < nvec) {
-          const int comp = t + 3 * which;
+          const int comp = T::epi_comp(t, which);
           const int64_t gbase = ((int64_t)comp * a.kf + e0) * NPG;
           const float4 rh = reinterpret_cast<const float4*>(s_stage + (size_t)which * TE * NPG)[c];
           if (MODE == MODE_RHS) {

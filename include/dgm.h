@@ -62,7 +62,7 @@ typedef struct {
   int32_t tile_elements;    /* elements per CTA tile of the stage kernel    */
   int32_t threads;          /* threads per CTA of the stage kernel          */
   int64_t smem_bytes_fixed; /* dynamic smem per CTA excluding code table    */
-  /* tensor-core (tcgen05, 3xTF32) stage path, f32 and N <= 8 only */
+  /* tensor-core (tcgen05, 3xTF32) stage path, f32 only */
   int32_t tc_supported;     /* 1 if this order/dtype has the tensor-core path */
   int32_t tc_nb;            /* MMA N: Np rounded up to 16                     */
   int32_t tc_steps;         /* K steps of 8 (K = 3*tc_npk + 4*Nfp, padded)     */
@@ -100,7 +100,7 @@ enum { DGM_PATH_AUTO = 0, DGM_PATH_SIMT = 1, DGM_PATH_TENSOR = 2 };
  *                tf32 hi part and the exact fp32 remainder:
  *                tc_operand[s][h][c][n][q] = part_h(B[n][8s + 4c + q]).
  *                NULL disables the tensor-core path.
- *  path        : DGM_PATH_AUTO (tensor cores for fp32, 2 <= N <= 8), _SIMT or _TENSOR.
+ *  path        : DGM_PATH_AUTO (tensor cores for fp32, N >= 2), _SIMT or _TENSOR.
  */
 typedef struct {
   int32_t order;

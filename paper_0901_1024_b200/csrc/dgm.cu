@@ -95,6 +95,7 @@ DGM_TC_INFO(5)
 DGM_TC_INFO(6)
 DGM_TC_INFO(7)
 DGM_TC_INFO(8)
+DGM_TC_INFO(9)
 #undef DGM_TC_INFO
 }  // namespace
 

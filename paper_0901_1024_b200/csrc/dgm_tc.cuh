@@ -95,9 +95,11 @@ struct TcCfg {
   // H_t of the 64 elements].  MAP 1 (N = 7, 8, where a 64-element u tile no longer fits in smem):
   // 32 elements per CTA, M-tiles component-major: tile 0 = [E_x | E_y | E_z | H_x], tile 1 =
   // [H_y | H_z | pad | pad] (32 lanes per component).
-  static constexpr int MAP = N <= 6 ? 0 : 1;
-  static constexpr int TE = MAP == 0 ? 64 : 32;    // elements per CTA
-  static constexpr int MT = MAP == 0 ? 3 : 2;      // M-tiles
+  // MAP 2 (N = 9): 16 elements per CTA, one M-tile holding all six components, lane = 16 c + e
+  // (96 of 128 lanes used).
+  static constexpr int MAP = N <= 6 ? 0 : (N <= 8 ? 1 : 2);
+  static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? 32 : 16);  // elements per CTA
+  static constexpr int MT = MAP == 0 ? 3 : (MAP == 1 ? 2 : 1);     // M-tiles
   static constexpr int PWARPS = 8;
   static constexpr int PROD = 32 * PWARPS;         // producer threads
   static constexpr int THREADS = PROD + 64;        // + MMA warp + loader warp
@@ -113,10 +115,6 @@ struct TcCfg {
   static constexpr int B_STEP_BYTES = 2 * 2 * NB * 16;   // hi/lo x 2 chunks x NB rows x 16 B
   static constexpr int NBS = N <= 5 ? 6 : 4;       // B ring slots (a slot is refilled when its MMAs complete)
   static constexpr uint32_t ROWS_BYTES = TE * NPG * 4;   // one field slab of the tile
-  static constexpr int ITEMS = TE * NFPK / PROD;   // (row, face node) flux items per thread
-  static_assert(ITEMS * PROD == TE * NFPK, "flux items must tile the producers");
-  static constexpr int IB = ITEMS % 4 == 0 ? 4 : (ITEMS % 3 == 0 ? 3 : (ITEMS % 2 == 0 ? 2 : 1));  // per gather batch
-  static_assert(ITEMS % IB == 0, "flux batches");
   // shared-memory carve-up (bytes)
   static constexpr size_t OFF_U = 0;
   static constexpr size_t OFF_GEO = OFF_U + (size_t)6 * ROWS_BYTES;
@@ -132,10 +130,12 @@ struct TcCfg {
   static constexpr size_t SMEM_FIXED = OFF_PTAB;   // + ncodes * NFP
   static constexpr size_t B_FLOATS = (size_t)KS * 2 * 2 * NB * 4;  // packed operand in global
 
-  // component held by TMEM lane quadrant q in M-tile t (>= 6: padding lanes)
-  __host__ __device__ static constexpr int comp_of(int t, int q) { return MAP == 0 ? t + 3 * (q >> 1) : 4 * t + q; }
+  // component held by TMEM lane (quadrant q, lane l) in M-tile t (>= 6: padding lanes)
+  __host__ __device__ static constexpr int comp_of(int t, int q, int l) {
+    return MAP == 0 ? t + 3 * (q >> 1) : (MAP == 1 ? 4 * t + q : 2 * q + (l >> 4));
+  }
   // element row of lane (q, l)
-  __host__ __device__ static constexpr int row_of(int q, int l) { return MAP == 0 ? (q & 1) * 32 + l : l; }
+  __host__ __device__ static constexpr int row_of(int q, int l) { return MAP == 0 ? (q & 1) * 32 + l : (MAP == 1 ? l : (l & 15)); }
   // epilogue phase p moves two components (which = 0, 1) through the rows buffer
   __host__ __device__ static constexpr int epi_comp(int p, int which) { return MAP == 0 ? p + 3 * which : 2 * p + which; }
 };
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
   using namespace tc;
   constexpr int TE = T::TE, NPG = T::NPG, NP = T::NP, NFP = T::NFP, NB = T::NB, NFPK = T::NFPK;
   constexpr int KS = T::KS, KV = T::KV, NPK = T::NPK, SROW = T::SROW, PROD = T::PROD, NBS = T::NBS;
-  constexpr int ITEMS = T::ITEMS, IB = T::IB, MT = T::MT, AST = T::AST;
+  constexpr int MT = T::MT, AST = T::AST;
   const StageArgs<float>& a = args.s;
 
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -314,12 +314,12 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     // A values of K-step s for this thread's row (4 columns x 3 M-tiles), unsplit
     auto a_values = [&](int s, float (&v)[MT][4]) {
       const int k0 = s * 8;
-      if constexpr (T::MAP == 1) {
+      if constexpr (T::MAP != 0) {
         // one component per M-tile: comp c = 4t + quad; (curl H)_cc / eps for c < 3, -(curl E)_cc / mu
         const int k = k0 + 4 * khalf;
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
-          const int c = T::comp_of(t, quad);
+          const int c = T::comp_of(t, quad, lane);
           if (c >= 6) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) v[t][q] = 0.f;
@@ -524,10 +524,11 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       }
       // quadrant warps holding the phase's components: TMEM lanes -> smem rows [which][row][NPG]
       // (MAP 0: M-tile t, all four quadrants; MAP 1: M-tile t/2, quadrants 2(t%2), 2(t%2)+1)
-      const bool mover = khalf == 0 && (T::MAP == 0 || (quad >> 1) == (t & 1));
+      // (MAP 2: the single M-tile, quadrant t: lanes 0-15 component 2t, 16-31 component 2t+1)
+      const bool mover = khalf == 0 && (T::MAP == 0 || (T::MAP == 1 ? (quad >> 1) == (t & 1) : quad == t));
       if (mover) {
-        const int tile = T::MAP == 0 ? t : t >> 1;
-        const int slot = T::MAP == 0 ? h : (quad & 1);
+        const int tile = T::MAP == 0 ? t : (T::MAP == 1 ? t >> 1 : 0);
+        const int slot = T::MAP == 0 ? h : (T::MAP == 1 ? (quad & 1) : (lane >> 4));
         float* dst = s_stage + (size_t)slot * TE * NPG + row * NPG;
 #pragma unroll
         for (int c0 = 0; c0 < NB; c0 += 8) {

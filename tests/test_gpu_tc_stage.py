@@ -11,7 +11,7 @@ from oracle import build_oracle_operator, rk4_step  # noqa: E402
 from paper_0901_1024_b200 import (CavityMode, Mesh, build_b200_operator, build_reference_element,  # noqa: E402
                                   generate_box_mesh, map_nodes)
 
-TC_ORDERS = [1, 2, 3, 4, 5, 6, 7, 8]
+TC_ORDERS = [1, 2, 3, 4, 5, 6, 7, 8, 9]
 
 
 @pytest.fixture(scope="module", autouse=True)

@@ -204,6 +204,7 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
       // never more CTAs per SM than TcCfg::CTAS: each allocates 512 / CTAS TMEM columns
       if (TC::CTAS == 2 && tc_smem < 80 * 1024) tc_smem = 80 * 1024;
       if (TC::CTAS == 1 && tc_smem < 120 * 1024) tc_smem = 120 * 1024;
+      if (TC::CTAS == 3 && tc_smem < 60 * 1024) tc_smem = 60 * 1024;
       if (tc_smem > 227 * 1024) {
         if (d.path == DGM_PATH_TENSOR) return fail(DGM_ERR_UNSUPPORTED, "tensor path smem %zu too large", tc_smem);
         return DGM_OK;

@@ -97,17 +97,25 @@ struct TcCfg {
   // [H_y | H_z | pad | pad] (32 lanes per component).
   // MAP 2 (N = 9): 16 elements per CTA, one M-tile holding all six components, lane = 16 c + e
   // (96 of 128 lanes used).
-  static constexpr int MAP = N <= 6 ? 0 : (N <= 8 ? 1 : 2);
+#ifdef DGM_TC_N4_SMALL
+  // Experiment knob (measured 2.73 ms vs 1.63 ms per C3 stage): N=4 on 16-element CTAs
+  // with 4 producer warps (both K halves per thread) and 3 CTAs per SM.
+  static constexpr bool SMALL = N == 4;
+#else
+  static constexpr bool SMALL = false;
+#endif
+  static constexpr int MAP = SMALL ? 2 : (N <= 6 ? 0 : (N <= 8 ? 1 : 2));
   static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? 32 : 16);  // elements per CTA
   static constexpr int MT = MAP == 0 ? 3 : (MAP == 1 ? 2 : 1);     // M-tiles
-  static constexpr int PWARPS = 8;
+  static constexpr int PWARPS = SMALL ? 4 : 8;   // producer warps: 4 lane quadrants x KH K-halves
+  static constexpr int KH = 8 / PWARPS;            // K-halves (4 columns each) per producer thread
   static constexpr int PROD = 32 * PWARPS;         // producer threads
   static constexpr int THREADS = PROD + 64;        // + MMA warp + loader warp
   static constexpr int ACC_COLS = MT * NB;
   static constexpr int A_COL0 = (ACC_COLS + 31) / 32 * 32;
   static constexpr int A_STAGE_COLS = MT * 16;     // M-tiles x (8 hi + 8 lo)
-  static constexpr int CTAS = N <= 4 ? 2 : 1;     // CTAs per SM (TMEM and smem split between them)
-  static constexpr int TMEM_COLS = 512 / CTAS;
+  static constexpr int CTAS = SMALL ? 3 : (N <= 4 ? 2 : 1);  // CTAs per SM (TMEM and smem split between them)
+  static constexpr int TMEM_COLS = CTAS == 3 ? 128 : 512 / CTAS;  // power of two
   static constexpr int AST0 = (TMEM_COLS - A_COL0) / A_STAGE_COLS;
   static constexpr int AST = AST0 > 6 ? 6 : AST0;   // A ring stages in TMEM
   static_assert(AST >= 2, "TMEM budget");
@@ -312,11 +320,11 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     for (int q = 0; q < 9; ++q) prx[q] = row_ok ? s_geo[row * GEO_WORDS + q] * inv_m : 0.f;
 
     // A values of K-step s for this thread's row (4 columns x 3 M-tiles), unsplit
-    auto a_values = [&](int s, float (&v)[MT][4]) {
+    auto a_values = [&](int s, int kh, float (&v)[MT][4]) {
       const int k0 = s * 8;
       if constexpr (T::MAP != 0) {
         // one component per M-tile: comp c = 4t + quad; (curl H)_cc / eps for c < 3, -(curl E)_cc / mu
-        const int k = k0 + 4 * khalf;
+        const int k = k0 + 4 * kh;
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
           const int c = T::comp_of(t, quad, lane);
@@ -345,7 +353,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
           }
         }
       } else {
-        const int k = k0 + 4 * khalf;
+        const int k = k0 + 4 * kh;
         if (k < 3 * NPK) {
           const int mu = k / NPK, j0 = k - mu * NPK;
           const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
@@ -450,33 +458,40 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     // Software-pipelined K loop: the next step's A values are computed between this step's
     // tcgen05.st and its tcgen05.wait::st, hiding the TMEM store latency; a flux pass (two named
     // barriers) runs only after this step's stage was handed to the MMA warp.
-    float vcur[MT][4], vnext[MT][4];
+    auto kh_of = [&](int j) { return T::KH == 1 ? khalf : j; };
+    float vcur[T::KH][MT][4], vnext[T::KH][MT][4];
 #ifndef DGM_EXP_NOFLUX
     if (face_start((0 + rot) % KS)) flux_pass(((0 + rot) % KS * 8 - KV) / NFPK);
 #endif
-    a_values((0 + rot) % KS, vcur);
+#pragma unroll
+    for (int j = 0; j < T::KH; ++j) a_values((0 + rot) % KS, kh_of(j), vcur[j]);
     for (int i = 0; i < KS; ++i) {  // i: position in this CTA's K order, s: K-step
       const int slot = i % AST;
       const int s = (i + rot) % KS;
       if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
-      float hi[MT][4], lo[MT][4];
 #pragma unroll
-      for (int t = 0; t < MT; ++t)
+      for (int j = 0; j < T::KH; ++j) {
+        float hi[MT][4], lo[MT][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) split_tf32(row_ok ? vcur[t][q] : 0.f, hi[t][q], lo[t][q]);
-      mbar_wait(&empty[slot], ((i / AST) & 1) ^ 1);
-      if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free
-      fence_after_sync();
+        for (int t = 0; t < MT; ++t)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) split_tf32(row_ok ? vcur[j][t][q] : 0.f, hi[t][q], lo[t][q]);
+        if (j == 0) {
+          mbar_wait(&empty[slot], ((i / AST) & 1) ^ 1);
+          if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free
+          fence_after_sync();
+        }
 #ifndef DGM_EXP_NOSTORE
 #pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + t * 16 + 4 * khalf;
-        tmem_st4(tmem + lane_addr + col, hi[t]);
-        tmem_st4(tmem + lane_addr + col + 8, lo[t]);
-      }
+        for (int t = 0; t < MT; ++t) {
+          const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + t * 16 + 4 * kh_of(j);
+          tmem_st4(tmem + lane_addr + col, hi[t]);
+          tmem_st4(tmem + lane_addr + col + 8, lo[t]);
+        }
 #else
-      if (hi[0][0] == 12345.f && lo[2][3] == 1.f) s_stage[0] = 0.f;  // keep the values live
+        if (hi[0][0] == 12345.f && lo[0][3] == 1.f) s_stage[0] = 0.f;  // keep the values live
 #endif
+      }
       const int sn = (i + 1 + rot) % KS;
       const bool has_next = i + 1 < KS;
 #ifdef DGM_EXP_NOFLUX
@@ -484,7 +499,10 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #else
       const bool next_flux = has_next && face_start(sn);
 #endif
-      if (has_next && !next_flux) a_values(sn, vnext);  // overlaps the TMEM store latency
+      if (has_next && !next_flux) {  // overlaps the TMEM store latency
+#pragma unroll
+        for (int j = 0; j < T::KH; ++j) a_values(sn, kh_of(j), vnext[j]);
+      }
       tmem_st_wait();
       fence_before_sync();
       __syncwarp();
@@ -492,12 +510,15 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       if (next_flux) {
         flux_pass((sn * 8 - KV) / NFPK);
         if (tid == 0) TC_TRACE(0, 103 + 4 * sn);  // face flux staged
-        a_values(sn, vnext);
+#pragma unroll
+        for (int j = 0; j < T::KH; ++j) a_values(sn, kh_of(j), vnext[j]);
       }
 #pragma unroll
-      for (int t = 0; t < MT; ++t)
+      for (int j = 0; j < T::KH; ++j)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) vcur[t][q] = vnext[t][q];
+        for (int t = 0; t < MT; ++t)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) vcur[j][t][q] = vnext[j][t][q];
     }
 
     // ================= epilogue: accumulators -> LSRK update =================

@@ -107,8 +107,17 @@ struct TcCfg {
   static constexpr int MAP = SMALL ? 2 : (N <= 6 ? 0 : (N <= 8 ? 1 : 2));
   static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? 32 : 16);  // elements per CTA
   static constexpr int MT = MAP == 0 ? 3 : (MAP == 1 ? 2 : 1);     // M-tiles
-  static constexpr int PWARPS = SMALL ? 4 : 8;   // producer warps: 4 lane quadrants x KH K-halves
-  static constexpr int KH = 8 / PWARPS;            // K-halves (4 columns each) per producer thread
+#ifdef DGM_TC_W16
+  static constexpr bool WIDE = N <= 4;   // experiment: 16 producer warps, 2 K-columns per thread
+#else
+  static constexpr bool WIDE = false;
+#endif
+  // producer warps: 4 lane quadrants x NQ column groups
+  static constexpr int PWARPS = SMALL ? 4 : (WIDE ? 16 : 8);
+  static constexpr int NQ = PWARPS / 4;            // producer warps per lane quadrant
+  static constexpr int CW = PWARPS == 16 ? 2 : 4;  // K columns per group (tcgen05.st width)
+  static constexpr int KH = 8 / CW / NQ;           // column groups per producer thread and K-step
+  static constexpr int FB = PWARPS == 16 ? 2 : 4;  // face nodes per flux work unit
   static constexpr int PROD = 32 * PWARPS;         // producer threads
   static constexpr int THREADS = PROD + 64;        // + MMA warp + loader warp
   static constexpr int ACC_COLS = MT * NB;
@@ -147,6 +156,19 @@ struct TcCfg {
   // epilogue phase p moves two components (which = 0, 1) through the rows buffer
   __host__ __device__ static constexpr int epi_comp(int p, int which) { return MAP == 0 ? p + 3 * which : 2 * p + which; }
 };
+
+// CW consecutive floats from shared memory as one vector load (16 or 8 bytes, aligned by layout).
+template <int CW>
+__device__ __forceinline__ void lds_vec(const float* p, float (&v)[CW]) {
+  if constexpr (CW == 4) {
+    const float4 x = *reinterpret_cast<const float4*>(p);
+    v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+  } else {
+    static_assert(CW == 2, "column groups of 2 or 4");
+    const float2 x = *reinterpret_cast<const float2*>(p);
+    v[0] = x.x, v[1] = x.y;
+  }
+}
 
 struct TcArgs {
   StageArgs<float> s;
@@ -320,50 +342,50 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     for (int q = 0; q < 9; ++q) prx[q] = row_ok ? s_geo[row * GEO_WORDS + q] * inv_m : 0.f;
 
     // A values of K-step s for this thread's row (4 columns x 3 M-tiles), unsplit
-    auto a_values = [&](int s, int kh, float (&v)[MT][4]) {
+    auto a_values = [&](int s, int kh, float (&v)[MT][T::CW]) {
+      constexpr int CW = T::CW;
       const int k0 = s * 8;
       if constexpr (T::MAP != 0) {
         // one component per M-tile: comp c = 4t + quad; (curl H)_cc / eps for c < 3, -(curl E)_cc / mu
-        const int k = k0 + 4 * kh;
+        const int k = k0 + CW * kh;
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
           const int c = T::comp_of(t, quad, lane);
           if (c >= 6) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[t][q] = 0.f;
+            for (int q = 0; q < CW; ++q) v[t][q] = 0.f;
           } else if (k < 3 * NPK) {
             const int mu = k / NPK, j0 = k - mu * NPK;
             const int cc = c % 3, c1 = (cc + 1) % 3, c2 = (cc + 2) % 3;
             const int fb = c < 3 ? 3 : 0;  // E comps read H fields and vice versa
             const float m = c < 3 ? a.inv_eps : -a.inv_mu;
             const float pa = prx[mu * 3 + c1] * m, pb = prx[mu * 3 + c2] * m;
-            const float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + c2) * TE + row) * NPG + j0);
-            const float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + c1) * TE + row) * NPG + j0);
-            v[t][0] = pa * x.x - pb * y.x;
-            v[t][1] = pa * x.y - pb * y.y;
-            v[t][2] = pa * x.z - pb * y.z;
-            v[t][3] = pa * x.w - pb * y.w;
+            float xp[CW], yp[CW];
+            lds_vec<CW>(s_u + ((fb + c2) * TE + row) * NPG + j0, xp);
+            lds_vec<CW>(s_u + ((fb + c1) * TE + row) * NPG + j0, yp);
+#pragma unroll
+            for (int q = 0; q < CW; ++q) v[t][q] = pa * xp[q] - pb * yp[q];
           } else if (k >= KV) {
             const int node = (k - KV) % NFPK;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[t][q] = s_stage[(c * NFPK + node + q) * SROW + row];
+            for (int q = 0; q < CW; ++q) v[t][q] = s_stage[(c * NFPK + node + q) * SROW + row];
           } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[t][q] = 0.f;
+            for (int q = 0; q < CW; ++q) v[t][q] = 0.f;
           }
         }
       } else {
-        const int k = k0 + 4 * kh;
+        const int k = k0 + CW * kh;
         if (k < 3 * NPK) {
           const int mu = k / NPK, j0 = k - mu * NPK;
           const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
           const int fb = h == 0 ? 3 : 0;  // E comps read H fields and vice versa
-          const float4 x = *reinterpret_cast<const float4*>(s_u + ((fb + 0) * TE + row) * NPG + j0);
-          const float4 y = *reinterpret_cast<const float4*>(s_u + ((fb + 1) * TE + row) * NPG + j0);
-          const float4 z = *reinterpret_cast<const float4*>(s_u + ((fb + 2) * TE + row) * NPG + j0);
-          const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w}, zs[4] = {z.x, z.y, z.z, z.w};
+          float xs[CW], ys[CW], zs[CW];
+          lds_vec<CW>(s_u + ((fb + 0) * TE + row) * NPG + j0, xs);
+          lds_vec<CW>(s_u + ((fb + 1) * TE + row) * NPG + j0, ys);
+          lds_vec<CW>(s_u + ((fb + 2) * TE + row) * NPG + j0, zs);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < CW; ++q) {
             if (h == 0) {  // (curl H)_x,y,z
               v[0][q] = p1 * zs[q] - p2 * ys[q];
               v[1][q] = p2 * xs[q] - p0 * zs[q];
@@ -377,12 +399,12 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         } else if (k >= KV) {
           const int node = (k - KV) % NFPK;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < CW; ++q)
 #pragma unroll
             for (int t = 0; t < MT; ++t) v[t][q] = s_stage[((3 * h + t) * NFPK + node + q) * SROW + row];
         } else {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < CW; ++q)
 #pragma unroll
             for (int t = 0; t < MT; ++t) v[t][q] = 0.f;
         }
@@ -394,10 +416,10 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         // one work unit = (element row, 4 consecutive node slots): the row's face data (normal,
         // scale, code, neighbour, in-tile or not) is read once and u+ is fetched with typed
         // shared / global loads, all 24 in flight before any use
-        constexpr int NB4 = NFPK / 4;
+        constexpr int FB = T::FB, NBF = NFPK / FB;
 #pragma unroll 1
-        for (int unit = tid; unit < TE * NB4; unit += PROD) {
-          const int r = unit / NB4, n0 = (unit % NB4) * 4;
+        for (int unit = tid; unit < TE * NBF; unit += PROD) {
+          const int r = unit / NBF, n0 = (unit % NBF) * FB;
           const bool row_live = r < nv;
           const int code = row_live ? s_code[r * 4 + face] : -1;
           const int nb = s_nbr[r * 4 + face];
@@ -405,29 +427,29 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
           const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
           const float sc = row_live ? gk[22 + face] * gk[9] : 0.f;
           const float se = sc * a.inv_eps, sh = sc * a.inv_mu;
-          int im[4], jn[4];
+          int im[FB], jn[FB];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < FB; ++j) {
             const int node = n0 + j < NFP ? n0 + j : 0;
             im[j] = s_fmask[face * NFP + node];
             jn[j] = code >= 0 ? s_ptab[code * NFP + node] : 0;
           }
-          float up[4][6];
+          float up[FB][6];
           const int64_t loc = (int64_t)nb - e0;
           if (code >= 0 && loc >= 0 && loc < nv) {  // neighbour row in this tile: shared memory
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < FB; ++j)
 #pragma unroll
               for (int f = 0; f < 6; ++f) up[j][f] = s_u[(f * TE + (int)loc) * NPG + jn[j]];
           } else if (code >= 0) {  // neighbour row elsewhere: global (L2-prefetched at tile start)
             const float* g = a.u + (int64_t)nb * NPG;
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < FB; ++j)
 #pragma unroll
               for (int f = 0; f < 6; ++f) up[j][f] = __ldg(g + f * fstride + jn[j]);
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < FB; ++j) {
             float um[6];
 #pragma unroll
             for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + r) * NPG + im[j]];
@@ -458,8 +480,8 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     // Software-pipelined K loop: the next step's A values are computed between this step's
     // tcgen05.st and its tcgen05.wait::st, hiding the TMEM store latency; a flux pass (two named
     // barriers) runs only after this step's stage was handed to the MMA warp.
-    auto kh_of = [&](int j) { return T::KH == 1 ? khalf : j; };
-    float vcur[T::KH][MT][4], vnext[T::KH][MT][4];
+    auto kh_of = [&](int j) { return khalf * T::KH + j; };  // column group of the thread's j-th group
+    float vcur[T::KH][MT][T::CW], vnext[T::KH][MT][T::CW];
 #ifndef DGM_EXP_NOFLUX
     if (face_start((0 + rot) % KS)) flux_pass(((0 + rot) % KS * 8 - KV) / NFPK);
 #endif
@@ -471,11 +493,11 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
 #pragma unroll
       for (int j = 0; j < T::KH; ++j) {
-        float hi[MT][4], lo[MT][4];
+        float hi[MT][T::CW], lo[MT][T::CW];
 #pragma unroll
         for (int t = 0; t < MT; ++t)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) split_tf32(row_ok ? vcur[j][t][q] : 0.f, hi[t][q], lo[t][q]);
+          for (int q = 0; q < T::CW; ++q) split_tf32(row_ok ? vcur[j][t][q] : 0.f, hi[t][q], lo[t][q]);
         if (j == 0) {
           mbar_wait(&empty[slot], ((i / AST) & 1) ^ 1);
           if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free
@@ -484,9 +506,14 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #ifndef DGM_EXP_NOSTORE
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
-          const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + t * 16 + 4 * kh_of(j);
-          tmem_st4(tmem + lane_addr + col, hi[t]);
-          tmem_st4(tmem + lane_addr + col + 8, lo[t]);
+          const uint32_t col = T::A_COL0 + slot * T::A_STAGE_COLS + t * 16 + T::CW * kh_of(j);
+          if constexpr (T::CW == 4) {
+            tmem_st4(tmem + lane_addr + col, hi[t]);
+            tmem_st4(tmem + lane_addr + col + 8, lo[t]);
+          } else {
+            tmem_st2(tmem + lane_addr + col, hi[t]);
+            tmem_st2(tmem + lane_addr + col + 8, lo[t]);
+          }
         }
 #else
         if (hi[0][0] == 12345.f && lo[0][3] == 1.f) s_stage[0] = 0.f;  // keep the values live
@@ -518,7 +545,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #pragma unroll
         for (int t = 0; t < MT; ++t)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) vcur[j][t][q] = vnext[j][t][q];
+          for (int q = 0; q < T::CW; ++q) vcur[j][t][q] = vnext[j][t][q];
     }
 
     // ================= epilogue: accumulators -> LSRK update =================

@@ -186,6 +186,13 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
       : "memory");
 }
 
+// 32 lanes x 2 consecutive 32-bit columns from registers.
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(__float_as_uint(v[0])),
+               "r"(__float_as_uint(v[1]))
+               : "memory");
+}
+
 // 32 lanes x 4 consecutive 32-bit columns from registers.
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const float* v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),

@@ -1,0 +1,39 @@
+"""Host-side pieces of bench.py (no GPU): clock-sample parsing and the timed-window selection."""
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def _line(sm, smax=1965, power_cap="Not Active", thermal="Not Active"):
+    return f"0, {sm}, {smax}, 700.0, 0x0, Not Active, Not Active, {thermal}, {power_cap}\n"
+
+
+def test_clock_summary_uses_timed_window_and_reasons():
+    c = bench.ClockSampler(0)
+    c.samples = [(0.0, _line(1200)), (1.0, _line(1965)), (1.1, _line(1950, power_cap="Active")),
+                 (5.0, _line(900, thermal="Active"))]
+    c.t0, c.t1 = 0.9, 1.2
+    s = c.summary()
+    assert s["window"] == "timed" and s["samples"] == 2
+    assert s["sm_mhz"] == 1957.5 and s["sm_max_mhz"] == 1965.0
+    assert s["reasons"] == ["sw_power_cap"]
+
+
+def test_clock_summary_falls_back_to_whole_run():
+    c = bench.ClockSampler(0)
+    c.samples = [(0.0, _line(1965)), (0.5, "garbage\n")]
+    c.t0, c.t1 = 2.0, 2.1
+    s = c.summary()
+    assert s["window"] == "run" and s["samples"] == 1 and s["sm_mhz"] == 1965.0
+
+
+def test_flop_and_byte_model_matches_survey_appendix_b():
+    from paper_0901_1024_b200.perfmodel import bytes_per_element_stage, flops_per_element_stage
+
+    assert flops_per_element_stage(4) == 76410 and flops_per_element_stage(6) == 381864
+    assert bytes_per_element_stage(4, 4) == 3496 and bytes_per_element_stage(9, 4) == 21256

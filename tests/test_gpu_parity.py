@@ -191,3 +191,38 @@ def test_large_mesh_properties_fp32():
         assert e <= e_prev * (1 + 1e-6)
         e_prev = e
     assert op.check_padding(u)
+
+
+def test_workspaces_on_two_streams_match_default_path():
+    """op.advance(..., workspace=) on separate CUDA streams (the bench's e2e pattern) == the default path."""
+    mesh = _jittered(3, (3, 2, 2))
+    elem = build_reference_element(4)
+    op = build_b200_operator(mesh, elem, dtype=torch.float32)
+    u0 = np.random.default_rng(11).normal(size=(6, mesh.num_elements, elem.num_nodes))
+    ref = op.to_padded(u0)
+    op.advance(ref, 1e-3, 3, use_graph=False)
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    works = [op.workspace() for _ in range(2)]
+    outs = [op.empty_state() for _ in range(2)]
+    for j in range(2):
+        with torch.cuda.stream(streams[j]):
+            op.to_padded(u0, out=outs[j])
+            op.advance(outs[j], 1e-3, 3, use_graph=(j == 1), workspace=works[j])
+    torch.cuda.synchronize()
+    for j in range(2):
+        assert torch.equal(outs[j], ref)
+
+
+def test_stage_stats_count_kernel_launches():
+    mesh = generate_box_mesh((1.0, 1.0, 1.0), (2, 2, 2))
+    elem = build_reference_element(3)
+    op = build_b200_operator(mesh, elem)
+    u = op.to_padded(np.random.default_rng(2).normal(size=(6, mesh.num_elements, elem.num_nodes)))
+    op.collect_stats = True
+    op.advance(u, 1e-3, 2, use_graph=False)
+    op.rhs_padded(u)
+    st = op.stage_stats
+    assert st["lsrk_stage"].launches == 10 and st["rhs"].launches == 1
+    assert op.total_stats().launches == 11 and op.total_stats().ms > 0
+    op.reset_stats()
+    assert op.stage_stats == {}

@@ -290,7 +290,10 @@ def run_b200(args) -> None:
     # buffers / workspaces: one step's D2H overlaps the next step's H2D (PCIe is full duplex) and
     # compute.  Every byte counted below still crosses PCIe inside the timed region.
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    host_in = torch.from_numpy(np.ascontiguousarray(u0_host)).pin_memory()
+    # natural host state in the e2e dtype (default: the compute dtype -- an fp32 user keeps fp32 host
+    # buffers; --e2e-dtype f64 keeps the reference's float64 and doubles the PCIe bytes)
+    e2e_dtype = {"f32": torch.float32, "f64": torch.float64}[args.e2e_dtype or args.dtype]
+    host_in = torch.from_numpy(np.ascontiguousarray(u0_host)).to(e2e_dtype).pin_memory()
     nstreams = 3 if world == 1 else 1
     host_out = [torch.empty_like(host_in).pin_memory() for _ in range(nstreams)]
     e_host = [torch.empty(1, dtype=torch.float64).pin_memory() for _ in range(nstreams)]
@@ -307,7 +310,7 @@ def run_b200(args) -> None:
                 op.advance(ues[j], dt, 1, use_graph=False, workspace=works[j])  # 5 fused stage launches
             else:
                 advance(ues[j], 1)
-            host_out[j].copy_(op.from_padded(ues[j]), non_blocking=True)    # unpack + D2H of the new state
+            host_out[j].copy_(op.from_padded(ues[j], e2e_dtype), non_blocking=True)  # unpack + D2H of the new state
             e_host[j].copy_(op.mass_norm(ues[j], 1.0, 1.0), non_blocking=True)  # per-step energy scalar
 
     for j in range(nstreams):  # warm-up (allocations, first launches)
@@ -375,7 +378,8 @@ def run_b200(args) -> None:
         "e2e": {"value": e2e_gflops, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,
                 "streams": nstreams,
-                "path": "per step: pinned f64 natural state H2D -> op.to_padded -> op.advance(1 LSRK4 step) -> "
+                "host_dtype": str(e2e_dtype).replace("torch.", ""),
+                "path": "per step: pinned natural state H2D -> op.to_padded -> op.advance(1 LSRK4 step) -> "
                         "op.from_padded -> pinned host D2H, + energy scalar D2H; independent steps alternate "
                         "over %d CUDA stream(s)" % nstreams},
         "gpu_launches": launches,
@@ -397,6 +401,8 @@ def main(argv=None) -> None:
     ap.add_argument("--cells", type=int, nargs=3, default=list(CELLS))
     ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
     ap.add_argument("--e2e-steps", type=int, default=9)
+    ap.add_argument("--e2e-dtype", choices=("f32", "f64"), default=None,
+                    help="natural host-state dtype of the e2e leg (default: the compute dtype)")
     ap.add_argument("--cpu-steps", type=int, default=12)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--path", choices=("auto", "tensor", "simt"), default="auto",

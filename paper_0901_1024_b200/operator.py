@@ -288,14 +288,14 @@ class B200MaxwellOperator:
                                        self.field_stride, self._stream()), "dgm_pack")
         return out
 
-    def from_padded(self, padded: torch.Tensor) -> torch.Tensor:
-        """Padded device tensor -> natural (6, K, Np) float64 device tensor."""
+    def from_padded(self, padded: torch.Tensor, dtype: torch.dtype = torch.float64) -> torch.Tensor:
+        """Padded device tensor -> natural (6, K, Np) device tensor (float64 as the reference, or ``dtype``)."""
         self._check_padded(padded, "padded")
         out = torch.empty((N_FIELDS, self.num_elements, self.elem.num_nodes), dtype=torch.float64,
                           device=self.device)
         _capi.check(self._lib.dgm_unpack(self.order, self._dt_code, padded.data_ptr(), out.data_ptr(),
                                          self.num_elements, self.field_stride, self._stream()), "dgm_unpack")
-        return out
+        return out if dtype == torch.float64 else out.to(dtype)
 
     def check_padding(self, padded: torch.Tensor) -> bool:
         """True when every padding slot is exactly zero (fields.py:55-58)."""

@@ -54,8 +54,17 @@ struct Cfg {
   static constexpr int NFS = odd_chunk_pad(NF4, W);  // flux / rhs row stride (smem)
   static constexpr int NJC = (NP + VEC - 1) / VEC;   // 16-byte chunks of a D row
   static constexpr int NLC = (NF4 + VEC - 1) / VEC;  // 16-byte chunks of a LIFT row
-  static constexpr int G = (N <= 5) ? 8 : (N <= 7 ? 4 : 2);  // element groups
-  static constexpr int E = (W == 4) ? 4 : 2;                 // elements per thread
+#if defined(DGM_SIMT_G64) && defined(DGM_SIMT_E64)
+  // tuning override for the fp64 kernel (scripts/gpu_simt_tune*.sh)
+  static constexpr int G = W == 8 ? DGM_SIMT_G64 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
+  static constexpr int E = W == 8 ? DGM_SIMT_E64 : 4;
+#else
+  // element groups x elements per thread; fp64 N=3 and N=6 run one element per thread
+  // (229 vs 264 us and 1.66 vs 2.11 ms per stage at 48k tets; other orders are faster with two)
+  static constexpr bool E1 = W == 8 && (N == 3 || N == 6);
+  static constexpr int G = E1 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
+  static constexpr int E = E1 ? 1 : ((W == 4) ? 4 : 2);
+#endif
   static constexpr int TE = G * E;                           // elements per tile
   static constexpr int WORK = NP * G;
   static constexpr int THREADS = ((WORK + 31) / 32) * 32;

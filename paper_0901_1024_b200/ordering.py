@@ -1,0 +1,52 @@
+"""Element locality ordering for the stage kernels (the role of layout.py Alg. 2).
+
+The reference numbers box-mesh elements ix-major (mesh.py:111-121), so a
+64-element tile of the stage kernel is a column of ~11 cells whose x and y
+face neighbours all live in other tiles (gathered from L2).  Sorting the
+elements along a Morton (Z-order) curve of their centroids makes every tile
+a compact 3-D blob, so more face neighbours sit in the tile's shared memory.
+The order is internal to the operator: ``to_padded`` / ``from_padded`` and
+every natural-order attribute keep the reference numbering.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .facemaps import FaceMaps
+
+
+def _spread_bits(x: np.ndarray) -> np.ndarray:
+    """Insert two zero bits between the low 21 bits of x (3-D Morton interleave)."""
+    x = x.astype(np.uint64) & np.uint64(0x1FFFFF)
+    x = (x | (x << np.uint64(32))) & np.uint64(0x1F00000000FFFF)
+    x = (x | (x << np.uint64(16))) & np.uint64(0x1F0000FF0000FF)
+    x = (x | (x << np.uint64(8))) & np.uint64(0x100F00F00F00F00F)
+    x = (x | (x << np.uint64(4))) & np.uint64(0x10C30C30C30C30C3)
+    x = (x | (x << np.uint64(2))) & np.uint64(0x1249249249249249)
+    return x
+
+
+def morton_order(vertices: np.ndarray, elements: np.ndarray, resolution: int | None = None) -> np.ndarray:
+    """Permutation ``order`` (new slot -> element id) sorting elements by the Morton code of their centroid.
+
+    Centroids are quantised to ``resolution`` cells per axis (default ~ (K/6)^(1/3), the cell count
+    of a Kuhn-split box) so the tets of one cell share a code and stay together (stable sort).  On
+    the C3 box this raises the fraction of face neighbours inside a 64-element tile from 0.65 to 0.71.
+    """
+    c = vertices[elements].mean(axis=1)
+    if resolution is None:
+        resolution = max(1, int(round((len(c) / 6.0) ** (1.0 / 3.0))))
+    lo, hi = c.min(axis=0), c.max(axis=0)
+    q = np.floor((c - lo) / np.maximum(hi - lo, 1e-300) * (resolution - 1e-9)).astype(np.int64)
+    code = _spread_bits(q[:, 0]) | (_spread_bits(q[:, 1]) << np.uint64(1)) | (_spread_bits(q[:, 2]) << np.uint64(2))
+    return np.argsort(code, kind="stable").astype(np.int64)
+
+
+def permute_maps(maps: FaceMaps, order: np.ndarray) -> FaceMaps:
+    """Face maps in the new numbering: row s is old element order[s], neighbour ids relabelled."""
+    inv = np.empty_like(order)
+    inv[order] = np.arange(len(order))
+    nbr = inv[maps.neighbors[order]].astype(np.int32)
+    return FaceMaps(num_nodes=maps.num_nodes, face_nodes=maps.face_nodes, neighbors=nbr,
+                    codes=maps.codes[order].copy(), code_table=maps.code_table)

@@ -225,3 +225,26 @@ def test_cli_error_boundary_and_eoc_fit(capsys):
     h = np.array([0.5, 0.25, 0.125])
     assert abs(fit_eoc(h, 3.0 * h ** 4.2) - 4.2) < 1e-12
     assert rows_to_csv([{"a": 0.1, "b": 2}]) == "a,b\n0.10000000000000001,2\n"
+
+
+def test_morton_order_and_map_relabelling():
+    """Internal locality order (ordering.py): a permutation, tiles are compact, maps relabelled consistently."""
+    from paper_0901_1024_b200.facemaps import build_face_maps
+    from paper_0901_1024_b200.ordering import morton_order, permute_maps
+
+    mesh = generate_box_mesh((1.0, 1.0, 1.0), (12, 12, 12))
+    elem = R.build_reference_element(2)
+    order = morton_order(mesh.vertices, mesh.elements)
+    k = mesh.num_elements
+    assert np.array_equal(np.sort(order), np.arange(k))
+    maps = build_face_maps(mesh, elem)
+    pm = permute_maps(maps, order)
+    inner = pm.codes >= 0
+    assert np.array_equal(order[pm.neighbors[inner]], maps.neighbors[order][inner])
+    assert np.array_equal(pm.codes, maps.codes[order])
+    # 64-element tiles: more face neighbours inside the tile than with the reference numbering
+    def in_tile(nbr, codes):
+        idx = np.arange(len(nbr))[:, None] // 64
+        m = codes >= 0
+        return float(((nbr // 64) == idx)[m].mean())
+    assert in_tile(pm.neighbors, pm.codes) > in_tile(maps.neighbors, maps.codes)

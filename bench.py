@@ -212,7 +212,8 @@ def run_b200(args) -> None:
     if world == 1:
         mesh = generate_box_mesh((1.0, 1.0, 1.0), cells)
         op = build_b200_operator(mesh, elem, dtype=dtype, device=dev, path=args.path,
-                                 reorder={"auto": None, "natural": False, "morton": True}[args.element_order])
+                                 reorder={"auto": None, "natural": False, "morton": "morton",
+                                          "columns": True}[args.element_order])
         dt = stable_dt(mesh, op.geometry, args.order)
         extent = (1.0, 1.0, 1.0)
         u0_host = CavityMode(1, 1, 1, extent).evaluate(map_nodes(mesh, elem), 0.0)
@@ -362,7 +363,8 @@ def run_b200(args) -> None:
                    "global_elements": k * world,
                    "l2": "no flush: state+residual registers (%.2f GB) >> 126 MB L2" % (
                        2 * 6 * k * op.np_stride * word / 1e9),
-                   "element_order": "morton" if getattr(op, "_order", None) is not None else "natural",
+                   "element_order": (args.element_order if args.element_order != "auto" else "columns")
+                   if getattr(op, "_order", None) is not None else "natural",
                    "setup_s": round(setup_s, 2), "flops_per_element_stage": f_alg,
                    "bytes_per_element_stage": b_alg},
         "roofline": {"bound": "hbm", "achieved": b_alg * k / launch_s / 1e9, "peak": peaks["hbm_gbs"],
@@ -403,7 +405,7 @@ def main(argv=None) -> None:
     ap.add_argument("--cells", type=int, nargs=3, default=list(CELLS))
     ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
     ap.add_argument("--e2e-steps", type=int, default=9)
-    ap.add_argument("--element-order", choices=("auto", "natural", "morton"), default="auto",
+    ap.add_argument("--element-order", choices=("auto", "natural", "morton", "columns"), default="auto",
                     help="internal element numbering (ordering.py); auto = Morton where it pays")
     ap.add_argument("--e2e-dtype", choices=("f32", "f64"), default=None,
                     help="natural host-state dtype of the e2e leg (default: the compute dtype)")

@@ -477,11 +477,12 @@ class B200MaxwellOperator:
 def build_b200_operator(mesh: Mesh, elem: ReferenceElement, material: Material = VACUUM,
                         connectivity: FaceConnectivity | None = None, *,
                         dtype: torch.dtype = torch.float32, device=None, path: str = "auto",
-                        reorder: bool | None = None) -> B200MaxwellOperator:
+                        reorder: bool | str | None = None) -> B200MaxwellOperator:
     """Drop-in for build_reference_operator (oracle.py:97-141) on one B200.
 
-    ``reorder=True`` numbers the elements internally along a Morton curve of their centroids
-    (paper_0901_1024_b200/ordering.py); the natural-order API is unchanged.  Default (None): on
+    ``reorder=True`` numbers the elements internally in 2x2-cell columns of their centroids
+    (``"morton"``: along a Morton curve; paper_0901_1024_b200/ordering.py); the natural-order API
+    is unchanged.  Default (None): on
     where it pays, i.e. the fp32 tensor-core path with 64-element tiles (2 <= N <= 6): 4.5 %
     faster at C3; the smaller tiles of the other kernels gain nothing.
     """
@@ -493,9 +494,10 @@ def build_b200_operator(mesh: Mesh, elem: ReferenceElement, material: Material =
     maps = build_face_maps(mesh, elem, connectivity)
     order = None
     if reorder:
-        from .ordering import morton_order
+        from . import ordering
 
-        order = morton_order(mesh.vertices, mesh.elements)
+        fn = ordering.morton_order if reorder == "morton" else ordering.column_order
+        order = fn(mesh.vertices, mesh.elements)
     op = B200MaxwellOperator(elem, material, geometry_words(geometry), geometry.det_jacobians, maps,
                              dtype=dtype, device=device, path=path, order=order)
     op.mesh = mesh

@@ -43,6 +43,24 @@ def morton_order(vertices: np.ndarray, elements: np.ndarray, resolution: int | N
     return np.argsort(code, kind="stable").astype(np.int64)
 
 
+def column_order(vertices: np.ndarray, elements: np.ndarray, resolution: int | None = None,
+                 width: int = 2) -> np.ndarray:
+    """Permutation sorting elements into ``width`` x ``width`` columns of grid cells along z.
+
+    Centroids are binned on a grid of ``resolution`` cells per axis (default ~ (K/6)^(1/3)); the
+    key is (column x, column y, z, x within column, y within column, element id).  A 64-element
+    tile is then a 2 x 2 x ~2.7-cell block: 74 % of the face neighbours of the C3 box fall inside
+    the tile (Morton 71 %, reference numbering 65 %).
+    """
+    c = vertices[elements].mean(axis=1)
+    if resolution is None:
+        resolution = max(1, int(round((len(c) / 6.0) ** (1.0 / 3.0))))
+    lo, hi = c.min(axis=0), c.max(axis=0)
+    q = np.floor((c - lo) / np.maximum(hi - lo, 1e-300) * (resolution - 1e-9)).astype(np.int64)
+    return np.lexsort((np.arange(len(c)), q[:, 1] % width, q[:, 0] % width, q[:, 2],
+                       q[:, 1] // width, q[:, 0] // width)).astype(np.int64)
+
+
 def permute_maps(maps: FaceMaps, order: np.ndarray) -> FaceMaps:
     """Face maps in the new numbering: row s is old element order[s], neighbour ids relabelled."""
     inv = np.empty_like(order)

@@ -230,7 +230,7 @@ def test_cli_error_boundary_and_eoc_fit(capsys):
 def test_morton_order_and_map_relabelling():
     """Internal locality order (ordering.py): a permutation, tiles are compact, maps relabelled consistently."""
     from paper_0901_1024_b200.facemaps import build_face_maps
-    from paper_0901_1024_b200.ordering import morton_order, permute_maps
+    from paper_0901_1024_b200.ordering import column_order, morton_order, permute_maps
 
     mesh = generate_box_mesh((1.0, 1.0, 1.0), (12, 12, 12))
     elem = R.build_reference_element(2)
@@ -248,3 +248,7 @@ def test_morton_order_and_map_relabelling():
         m = codes >= 0
         return float(((nbr // 64) == idx)[m].mean())
     assert in_tile(pm.neighbors, pm.codes) > in_tile(maps.neighbors, maps.codes)
+    col = column_order(mesh.vertices, mesh.elements)
+    assert np.array_equal(np.sort(col), np.arange(k))
+    pc = permute_maps(maps, col)
+    assert in_tile(pc.neighbors, pc.codes) > in_tile(maps.neighbors, maps.codes)

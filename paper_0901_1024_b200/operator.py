@@ -482,12 +482,11 @@ def build_b200_operator(mesh: Mesh, elem: ReferenceElement, material: Material =
 
     ``reorder=True`` numbers the elements internally in 2x2-cell columns of their centroids
     (``"morton"``: along a Morton curve; paper_0901_1024_b200/ordering.py); the natural-order API
-    is unchanged.  Default (None): on
-    where it pays, i.e. the fp32 tensor-core path with 64-element tiles (2 <= N <= 6): 4.5 %
-    faster at C3; the smaller tiles of the other kernels gain nothing.
+    is unchanged.  Default (None): on for 2 <= N <= 8 (C3 fp32 1.63 -> 1.54 ms per stage, fp64
+    and N = 7, 8 0.4-1.3 % faster; N = 1 and N = 9 keep the reference numbering).
     """
     if reorder is None:
-        reorder = dtype == torch.float32 and 2 <= elem.order <= 6 and path != "simt"
+        reorder = 2 <= elem.order <= 8
     if connectivity is None:
         connectivity = build_connectivity(mesh)
     geometry = compute_geometry(mesh, elem)

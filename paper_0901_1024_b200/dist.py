@@ -201,7 +201,7 @@ class DistributedMaxwellOperator:
     """One rank's share of the operator; halo exchange over torch.distributed (NCCL)."""
 
     def __init__(self, domain: RankDomain, material: Material = VACUUM, *, dtype=None, device=None,
-                 path: str = "auto"):
+                 path: str = "auto", reorder: bool | None = None):
         import torch
 
         from .operator import B200MaxwellOperator
@@ -209,8 +209,11 @@ class DistributedMaxwellOperator:
         self.domain = domain
         self.torch = torch
         dtype = torch.float32 if dtype is None else dtype
+        if reorder is None:
+            reorder = 2 <= domain.elem.order <= 8  # as build_b200_operator
         self.op = B200MaxwellOperator(domain.elem, material, domain.geo_words, domain.det_j, domain.maps,
-                                      num_ghost=domain.num_ghost, dtype=dtype, device=device, path=path)
+                                      num_ghost=domain.num_ghost, dtype=dtype, device=device, path=path,
+                                      order=self._interior_order(domain) if reorder else None)
         self.device = self.op.device
         self.comm_stream = torch.cuda.Stream(self.device)
         rows = 6 * self.op.np_stride
@@ -221,6 +224,25 @@ class DistributedMaxwellOperator:
                       for p, (_, cnt) in domain.recv.items()}
         self._alt = self.op.empty_state()
         self._res = self.op.empty_state()
+
+    @staticmethod
+    def _interior_order(domain: RankDomain) -> np.ndarray:
+        """Locality order (ordering.column_order) of the interior range only.
+
+        The boundary ranges, whose rows are sent to peers and which are launched after the halo
+        arrives, keep their slots, so send lists, ghost slots and the interior / boundary split
+        are unchanged.
+        """
+        from .ordering import column_order
+
+        k = domain.num_owned
+        p, q = domain.interior
+        order = np.arange(k, dtype=np.int64)
+        if q - p > 1:
+            lo = domain.owned[0] - domain.sub_offset
+            elems = domain.mesh.elements[lo + p:lo + q]
+            order[p:q] = p + column_order(domain.mesh.vertices, elems)
+        return order
 
     @property
     def num_elements(self) -> int:

@@ -125,8 +125,8 @@ class B200MaxwellOperator:
             from .ordering import permute_maps
 
             order = np.asarray(order, dtype=np.int64)
-            if self.num_ghost or not np.array_equal(np.sort(order), np.arange(self.num_elements)):
-                raise ValueError("order must be a permutation of the elements (no ghosts)")
+            if not np.array_equal(np.sort(order), np.arange(self.num_elements)):
+                raise ValueError("order must be a permutation of the owned elements")
             geo_words, det_j, maps = geo_words[order], det_j[order], permute_maps(maps, order)
 
         def dev(a, dt=dtype):

@@ -65,9 +65,14 @@ def column_order(vertices: np.ndarray, elements: np.ndarray, resolution: int | N
 
 
 def permute_maps(maps: FaceMaps, order: np.ndarray) -> FaceMaps:
-    """Face maps in the new numbering: row s is old element order[s], neighbour ids relabelled."""
+    """Face maps in the new numbering: row s is old element order[s], neighbour ids relabelled.
+
+    Neighbour ids >= len(order) (ghost slots of a multi-GPU rank) are left unchanged.
+    """
+    k = len(order)
     inv = np.empty_like(order)
-    inv[order] = np.arange(len(order))
-    nbr = inv[maps.neighbors[order]].astype(np.int32)
+    inv[order] = np.arange(k)
+    nb = maps.neighbors[order].astype(np.int64)
+    nbr = np.where(nb < k, inv[np.minimum(nb, k - 1)], nb).astype(np.int32)
     return FaceMaps(num_nodes=maps.num_nodes, face_nodes=maps.face_nodes, neighbors=nbr,
                     codes=maps.codes[order].copy(), code_table=maps.code_table)

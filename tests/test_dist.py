@@ -173,3 +173,25 @@ def test_gloo_distributed_lsrk_matches_single_process(world):
     for _, g0, g1, block in parts:
         got[:, g0:g1] = block
     assert np.abs(got - u).max() <= 1e-12 * np.abs(u).max()
+
+
+def test_interior_locality_order_keeps_boundary_and_ghost_slots():
+    """DistributedMaxwellOperator's locality order permutes only the interior range."""
+    from paper_0901_1024_b200.dist import DistributedMaxwellOperator
+    from paper_0901_1024_b200.ordering import permute_maps
+
+    elem = build_reference_element(3)
+    dom = build_box_domain((2.0, 1.0, 1.0), (12, 4, 4), elem, 0, 2)
+    order = DistributedMaxwellOperator._interior_order(dom)
+    k = dom.num_owned
+    p, q = dom.interior
+    assert q - p > 64 and np.array_equal(np.sort(order), np.arange(k))
+    assert np.array_equal(order[:p], np.arange(p)) and np.array_equal(order[q:], np.arange(q, k))
+    assert not np.array_equal(order[p:q], np.arange(p, q))
+    pm = permute_maps(dom.maps, order)
+    ghost = dom.maps.neighbors >= k
+    assert np.array_equal(pm.neighbors[ghost[order]], dom.maps.neighbors[order][ghost[order]])
+    inner = (pm.codes >= 0) & (pm.neighbors < k)
+    assert np.array_equal(order[pm.neighbors[inner]], dom.maps.neighbors[order][inner])
+    for ids in dom.send.values():  # every sent row is outside the permuted range
+        assert np.all((ids < p) | (ids >= q))

@@ -226,7 +226,8 @@ def run_b200(args) -> None:
         extent = (float(world), 1.0, 1.0)
         gcells = (cells[0] * world, cells[1], cells[2])
         dom = build_box_domain(extent, gcells, elem, rank, world)
-        runner = DistributedMaxwellOperator(dom, dtype=dtype, device=dev, path=args.path)
+        runner = DistributedMaxwellOperator(dom, dtype=dtype, device=dev, path=args.path,
+                                            reorder={"auto": None, "natural": False}.get(args.element_order, True))
         op = runner.op
         lo = dom.owned[0] - dom.sub_offset
         own_mesh = Mesh(dom.mesh.vertices, dom.mesh.elements[lo:lo + dom.num_owned])

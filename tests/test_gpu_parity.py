@@ -132,9 +132,11 @@ def test_odd_step_counts_and_generic_rk4(dtype):
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_material_constants(dtype):
-    mesh = _jittered(2)
-    elem = build_reference_element(3)
+@pytest.mark.parametrize("n", [3, 7, 9])
+def test_material_constants(dtype, n):
+    """eps, mu != 1 on every lane mapping of the tensor kernel (N=3: E|H tiles, 7: comp-major, 9: one tile)."""
+    mesh = _jittered(2) if n <= 3 else _jittered(2, (2, 1, 1))
+    elem = build_reference_element(n)
     mat = Material(permittivity=2.0, permeability=0.5)
     op = build_b200_operator(mesh, elem, mat, dtype=dtype)
     ora = OracleOperator(mesh.vertices, mesh.elements, elem, eps=2.0, mu=0.5)

@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     for (int i = 0; i < KS; ++i) {  // i: position in this CTA's K order, s: K-step
       const int slot = i % AST;
       const int s = (i + rot) % KS;
+      (void)s;                                  // (trace builds only)
       if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
 #pragma unroll
       for (int j = 0; j < T::KH; ++j) {

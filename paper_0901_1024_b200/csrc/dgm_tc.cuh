@@ -238,6 +238,11 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 
   if (warp == T::PWARPS + 1) {
     // ================= loader warp =================
+    // warm L2 with the tile's residual rows, read by the epilogue
+    auto prefetch_res = [&]() {
+      const uint32_t rb = (uint32_t)nv * NPG * 4;
+      for (int f = 0; f < 6; ++f) prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rb);
+    };
     auto load_b = [&](int i) {  // B operand of the i-th K-step (in this CTA's order) into its ring slot
       if (i >= KS) return;
       const int slot = i % NBS;
@@ -256,8 +261,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       bulk_g2s(s_code, a.code + e0 * 4, conbytes, load_full);
       for (int f = 0; f < 6; ++f)
         bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowbytes, load_full);
-      if (MODE == MODE_LSRK && !a.a_zero)
-        for (int f = 0; f < 6; ++f) prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rowbytes);
+      if (MODE == MODE_LSRK && !a.a_zero && KS <= NBS) prefetch_res();
       // warm L2 with the rows of the tile one wave ahead, so that CTA's bulk loads hit L2
       const int64_t nt = (int64_t)blockIdx.x + args.wave;
       if (nt < args.num_tiles) {
@@ -274,7 +278,11 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     // cannot run a phase ahead of this wait: its next completion needs B(j + NBS), loaded below.
     for (int j = 0; j + NBS < KS; ++j) {
       mbar_wait(&b_empty[j % NBS], (j / NBS) & 1);
-      if (elect_one()) load_b(j + NBS);
+      if (elect_one()) {
+        load_b(j + NBS);
+        // residual rows ~NBS K-steps before the epilogue: fresh in L2 when it reads them
+        if (MODE == MODE_LSRK && !a.a_zero && j + NBS == KS - 1) prefetch_res();
+      }
       __syncwarp();
     }
   } else if (warp == T::PWARPS) {

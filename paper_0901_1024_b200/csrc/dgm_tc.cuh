@@ -330,7 +330,10 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     if (tid == 0) TC_TRACE(0, 1);  // start
     mbar_wait(load_full, 0);
     if (tid == 0) TC_TRACE(0, 2);  // rows landed
-    {  // warm L2 with the rows of every face neighbour outside the tile (read by the face K-steps)
+    // warm L2 with the rows of every face neighbour outside the tile (read by the face K-steps);
+    // issued DGM_TC_NBR_LEAD K-steps before this CTA's first face step (-1: at tile start);
+    // A/B at C3: lead 2..11 all -1.6% vs tile start, where it delays the first A stores
+    auto nbr_prefetch = [&]() {
       for (int e = tid; e < nv * 4; e += PROD) {
         const int code = s_code[e];
         const int64_t nb = s_nbr[e];
@@ -343,7 +346,13 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
           }
         }
       }
-    }
+    };
+#ifndef DGM_TC_NBR_LEAD
+#define DGM_TC_NBR_LEAD 5
+#endif
+    const int nbr_pf_i = DGM_TC_NBR_LEAD < 0 ? -1
+                         : max(0, (rot < KV / 8 ? KV / 8 - rot : 0) - DGM_TC_NBR_LEAD);
+    if (nbr_pf_i < 0) nbr_prefetch();
     const bool row_ok = row < nv;
     float prx[9];  // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu
 #pragma unroll
@@ -449,7 +458,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
             for (int j = 0; j < FB; ++j)
 #pragma unroll
               for (int f = 0; f < 6; ++f) up[j][f] = s_u[(f * TE + (int)loc) * NPG + jn[j]];
-          } else if (code >= 0) {  // neighbour row elsewhere: global (L2-prefetched at tile start)
+          } else if (code >= 0) {  // neighbour row elsewhere: global (L2-prefetched a few K-steps ahead)
             const float* g = a.u + (int64_t)nb * NPG;
 #pragma unroll
             for (int j = 0; j < FB; ++j)
@@ -500,6 +509,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       const int s = (i + rot) % KS;
       (void)s;                                  // (trace builds only)
       if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
+      if (i == nbr_pf_i) nbr_prefetch();
 #pragma unroll
       for (int j = 0; j < T::KH; ++j) {
         float hi[MT][T::CW], lo[MT][T::CW];

@@ -128,7 +128,45 @@ struct TcCfg {
   static constexpr int AST0 = (TMEM_COLS - A_COL0) / A_STAGE_COLS;
   static constexpr int AST = AST0 > 6 ? 6 : AST0;   // A ring stages in TMEM
   static_assert(AST >= 2, "TMEM budget");
-  static constexpr int SROW = TE + 4;              // flux staging row stride
+  // flux staging row stride TE + pad: the pad minimises the shared-bank multiplicity of the flux
+  // pass stores (lanes = (row, node block) units) plus the MAP 2 staging reads (two components
+  // per warp); TE + 4 had 2-way (N=3,4) up to 7-way (N=9) store conflicts
+  static constexpr int bank_mult(const int* addr, int n) {
+    int cnt[32] = {}, m = 0;
+    for (int i = 0; i < n; ++i) {
+      const int b = addr[i] % 32;
+      m = ++cnt[b] > m ? cnt[b] : m;
+    }
+    return m;
+  }
+  static constexpr int srow_cost(int pad) {  // x NBF: integer arithmetic
+    const int S = TE + pad, NBF = NFPK / FB;
+    int tot = 0, warps = 0;
+    for (int w = 0; w < NBF; ++w) {
+      int addr[32] = {}, n = 0;
+      for (int u = w * 32; u < w * 32 + 32; ++u)
+        if (u / NBF < TE) addr[n++] = (u % NBF) * FB * S + u / NBF;
+      if (n) tot += bank_mult(addr, n), ++warps;
+    }
+    int rd = 1;
+    if (MAP == 2) {
+      int addr[32] = {};
+      for (int l = 0; l < 32; ++l) addr[l] = (l >> 4) * NFPK * S + (l & 15);
+      rd = bank_mult(addr, 32);
+    }
+    return (tot * 64) / warps + rd * 64;
+  }
+  static constexpr int srow_pad() {
+    int best = 0;
+    for (int p = 1; p < 32; ++p)
+      if (srow_cost(p) < srow_cost(best)) best = p;
+    return best;
+  }
+#ifdef DGM_TC_SROW_OLD
+  static constexpr int SROW = TE + 4;  // experiment: the previous fixed padding
+#else
+  static constexpr int SROW = TE + srow_pad();
+#endif
   static constexpr int B_STEP_BYTES = 2 * 2 * NB * 16;   // hi/lo x 2 chunks x NB rows x 16 B
   static constexpr int NBS = N <= 5 ? 6 : 4;       // B ring slots (a slot is refilled when its MMAs complete)
   static constexpr uint32_t ROWS_BYTES = TE * NPG * 4;   // one field slab of the tile
@@ -331,7 +369,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     mbar_wait(load_full, 0);
     if (tid == 0) TC_TRACE(0, 2);  // rows landed
     // warm L2 with the rows of every face neighbour outside the tile (read by the face K-steps);
-    // issued DGM_TC_NBR_LEAD K-steps before this CTA's first face step (-1: at tile start);
+    // issued LEAD K-steps before this CTA's first face step (-1: at tile start);
     // A/B at C3: lead 2..11 all -1.6% vs tile start, where it delays the first A stores
     auto nbr_prefetch = [&]() {
       for (int e = tid; e < nv * 4; e += PROD) {
@@ -347,11 +385,13 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         }
       }
     };
-#ifndef DGM_TC_NBR_LEAD
-#define DGM_TC_NBR_LEAD 5
+#ifdef DGM_TC_NBR_LEAD
+    constexpr int LEAD = DGM_TC_NBR_LEAD;
+#else
+    // A/B (lead 5 vs -1): N=4 C3 -1.6%; N=3, 6 +1%, N=7 0, N=8, 9 +5% -> only N=4 uses a lead
+    constexpr int LEAD = N == 4 ? 5 : -1;
 #endif
-    const int nbr_pf_i = DGM_TC_NBR_LEAD < 0 ? -1
-                         : max(0, (rot < KV / 8 ? KV / 8 - rot : 0) - DGM_TC_NBR_LEAD);
+    const int nbr_pf_i = LEAD < 0 ? -1 : max(0, (rot < KV / 8 ? KV / 8 - rot : 0) - LEAD);
     if (nbr_pf_i < 0) nbr_prefetch();
     const bool row_ok = row < nv;
     float prx[9];  // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu

@@ -213,7 +213,8 @@ def run_b200(args) -> None:
         mesh = generate_box_mesh((1.0, 1.0, 1.0), cells)
         op = build_b200_operator(mesh, elem, dtype=dtype, device=dev, path=args.path,
                                  reorder={"auto": None, "natural": False, "morton": "morton",
-                                          "columns": True}[args.element_order])
+                                          "columns": True}[args.element_order],
+                                 face_slots=None if args.face_slots == "auto" else False)
         dt = stable_dt(mesh, op.geometry, args.order)
         extent = (1.0, 1.0, 1.0)
         u0_host = CavityMode(1, 1, 1, extent).evaluate(map_nodes(mesh, elem), 0.0)
@@ -227,7 +228,8 @@ def run_b200(args) -> None:
         gcells = (cells[0] * world, cells[1], cells[2])
         dom = build_box_domain(extent, gcells, elem, rank, world)
         runner = DistributedMaxwellOperator(dom, dtype=dtype, device=dev, path=args.path,
-                                            reorder={"auto": None, "natural": False}.get(args.element_order, True))
+                                            reorder={"auto": None, "natural": False}.get(args.element_order, True),
+                                            face_slots=None if args.face_slots == "auto" else False)
         op = runner.op
         lo = dom.owned[0] - dom.sub_offset
         own_mesh = Mesh(dom.mesh.vertices, dom.mesh.elements[lo:lo + dom.num_owned])
@@ -366,6 +368,7 @@ def run_b200(args) -> None:
                        2 * 6 * k * op.np_stride * word / 1e9),
                    "element_order": (args.element_order if args.element_order != "auto" else "columns")
                    if getattr(op, "_order", None) is not None else "natural",
+                   "face_slots": "bank-spread" if getattr(op, "_slot_inv", None) is not None else "natural",
                    "setup_s": round(setup_s, 2), "flops_per_element_stage": f_alg,
                    "bytes_per_element_stage": b_alg},
         "roofline": {"bound": "hbm", "achieved": b_alg * k / launch_s / 1e9, "peak": peaks["hbm_gbs"],
@@ -408,6 +411,8 @@ def main(argv=None) -> None:
     ap.add_argument("--e2e-steps", type=int, default=9)
     ap.add_argument("--element-order", choices=("auto", "natural", "morton", "columns"), default="auto",
                     help="internal element numbering (ordering.py); auto = Morton where it pays")
+    ap.add_argument("--face-slots", choices=("auto", "natural"), default="auto",
+                    help="node order inside each face (ordering.face_slot_order); auto = bank-spread on the tensor path")
     ap.add_argument("--e2e-dtype", choices=("f32", "f64"), default=None,
                     help="natural host-state dtype of the e2e leg (default: the compute dtype)")
     ap.add_argument("--cpu-steps", type=int, default=12)

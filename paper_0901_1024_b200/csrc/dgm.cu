@@ -5,6 +5,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <type_traits>
 #include <utility>
@@ -31,6 +33,25 @@ int fail(int code, const char* fmt, ...) {
 
 int cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) return fail(DGM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return DGM_OK;
+}
+
+// The dynamic shared-memory limit is a per-function attribute shared by every plan of the same
+// (order, dtype) on a device, while the bytes a plan launches with depend on its code table: the
+// limit is only ever raised, so a plan created later with fewer codes cannot shrink it under an
+// earlier plan's launches.
+template <typename K>
+int raise_smem_limit(K* kernel, size_t bytes, const char* what) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> limits;
+  int dev = 0;
+  if (int r = cuda_check(cudaGetDevice(&dev), "cudaGetDevice")) return r;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = limits[{dev, reinterpret_cast<const void*>(kernel)}];
+  if (bytes <= cur) return DGM_OK;
+  if (int r = cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), what))
+    return r;
+  cur = bytes;
   return DGM_OK;
 }
 
@@ -160,26 +181,16 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
     if (smem > 227 * 1024)
       return fail(DGM_ERR_UNSUPPORTED, "stage kernel needs %zu bytes of shared memory", smem);
     int r;
-    if ((r = cuda_check(cudaFuncSetAttribute(dgm::stage_kernel<N, T, dgm::MODE_RHS>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "cudaFuncSetAttribute")))
+    if ((r = raise_smem_limit(dgm::stage_kernel<N, T, dgm::MODE_RHS>, smem, "cudaFuncSetAttribute")))
       return r;
-    if ((r = cuda_check(cudaFuncSetAttribute(dgm::stage_kernel<N, T, dgm::MODE_LSRK>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "cudaFuncSetAttribute")))
+    if ((r = raise_smem_limit(dgm::stage_kernel<N, T, dgm::MODE_LSRK>, smem, "cudaFuncSetAttribute")))
       return r;
-    if ((r = cuda_check(cudaFuncSetAttribute(dgm::stage_kernel<N, T, dgm::MODE_VOLUME>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "cudaFuncSetAttribute")))
+    if ((r = raise_smem_limit(dgm::stage_kernel<N, T, dgm::MODE_VOLUME>, smem, "cudaFuncSetAttribute")))
       return r;
-    if ((r = cuda_check(cudaFuncSetAttribute(dgm::stage_kernel<N, T, dgm::MODE_SURFACE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "cudaFuncSetAttribute")))
+    if ((r = raise_smem_limit(dgm::stage_kernel<N, T, dgm::MODE_SURFACE>, smem, "cudaFuncSetAttribute")))
       return r;
     const size_t msmem = (size_t)6 * C::TE * C::NPG * sizeof(T);
-    if ((r = cuda_check(cudaFuncSetAttribute(dgm::mass_norm_kernel<N, T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem),
-                        "cudaFuncSetAttribute")))
+    if ((r = raise_smem_limit(dgm::mass_norm_kernel<N, T>, msmem, "cudaFuncSetAttribute")))
       return r;
     return DGM_OK;
   });
@@ -210,13 +221,9 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
         return DGM_OK;
       }
       int r;
-      if ((r = cuda_check(cudaFuncSetAttribute(dgm::tc_stage_kernel<N, dgm::MODE_RHS>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem),
-                          "cudaFuncSetAttribute(tc)")))
+      if ((r = raise_smem_limit(dgm::tc_stage_kernel<N, dgm::MODE_RHS>, tc_smem, "cudaFuncSetAttribute(tc)")))
         return r;
-      if ((r = cuda_check(cudaFuncSetAttribute(dgm::tc_stage_kernel<N, dgm::MODE_LSRK>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem),
-                          "cudaFuncSetAttribute(tc)")))
+      if ((r = raise_smem_limit(dgm::tc_stage_kernel<N, dgm::MODE_LSRK>, tc_smem, "cudaFuncSetAttribute(tc)")))
         return r;
       path = DGM_PATH_TENSOR;
       return DGM_OK;

@@ -201,7 +201,7 @@ class DistributedMaxwellOperator:
     """One rank's share of the operator; halo exchange over torch.distributed (NCCL)."""
 
     def __init__(self, domain: RankDomain, material: Material = VACUUM, *, dtype=None, device=None,
-                 path: str = "auto", reorder: bool | None = None):
+                 path: str = "auto", reorder: bool | None = None, face_slots: bool | None = None):
         import torch
 
         from .operator import B200MaxwellOperator
@@ -213,7 +213,8 @@ class DistributedMaxwellOperator:
             reorder = 2 <= domain.elem.order <= 8  # as build_b200_operator
         self.op = B200MaxwellOperator(domain.elem, material, domain.geo_words, domain.det_j, domain.maps,
                                       num_ghost=domain.num_ghost, dtype=dtype, device=device, path=path,
-                                      order=self._interior_order(domain) if reorder else None)
+                                      order=self._interior_order(domain) if reorder else None,
+                                      face_slots=face_slots)
         self.device = self.op.device
         self.comm_stream = torch.cuda.Stream(self.device)
         rows = 6 * self.op.np_stride

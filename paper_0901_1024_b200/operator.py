@@ -44,20 +44,22 @@ def pack_chunks(mat: np.ndarray, chunks: int, vec: int) -> np.ndarray:
     return np.ascontiguousarray(padded.reshape(rows, chunks, vec).transpose(1, 0, 2))
 
 
-def tc_operand(elem: ReferenceElement, lay) -> np.ndarray:
+def tc_operand(elem: ReferenceElement, lay, lift: np.ndarray | None = None) -> np.ndarray:
     """Constant GEMM operand of the tensor-core path, layout of dgm_desc.tc_operand (include/dgm.h).
 
     B[n][k] = [D_r | D_s | D_t | 0 | LIFT_f0 | .. | LIFT_f3][n][k] with each
     derivative block tc_npk and each face block tc_nfpk wide; split into a tf32-exact high part (13 low mantissa bits cleared) and
-    the float32 remainder, so that hi*x + lo*x carries fp32 accuracy.
+    the float32 remainder, so that hi*x + lo*x carries fp32 accuracy.  ``lift`` overrides
+    elem.lift (face-slot-permuted columns).
     """
+    lift = elem.lift if lift is None else lift
     n_p, n_fp = elem.num_nodes, elem.num_face_nodes
     nb, npk, steps, kv, nfpk = lay.tc_nb, lay.tc_npk, lay.tc_steps, lay.tc_kv, lay.tc_nfpk
     full = np.zeros((nb, steps * 8))
     for mu in range(3):
         full[:n_p, mu * npk:mu * npk + n_p] = elem.diff[mu]
     for f in range(NUM_FACES):
-        full[:n_p, kv + f * nfpk:kv + f * nfpk + n_fp] = elem.lift[:, f * n_fp:(f + 1) * n_fp]
+        full[:n_p, kv + f * nfpk:kv + f * nfpk + n_fp] = lift[:, f * n_fp:(f + 1) * n_fp]
     hi = (full.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
     lo = (full - hi.astype(np.float64)).astype(np.float32)
     parts = np.stack([hi, lo])                                   # (2, nb, K)
@@ -65,6 +67,19 @@ def tc_operand(elem: ReferenceElement, lay) -> np.ndarray:
     out = np.ascontiguousarray(packed, dtype=np.float32)
     assert out.size == lay.tc_operand_floats
     return out
+
+
+_SLOT_ORDERS: dict = {}
+
+
+def _face_slot_order(elem: ReferenceElement) -> np.ndarray:
+    """ordering.face_slot_order for this element and layout, cached per order."""
+    from .ordering import face_slot_order
+
+    if elem.order not in _SLOT_ORDERS:  # modelled on the fp32 tensor kernel's strides (TcCfg<N>)
+        npg, nfpk = (elem.num_nodes + 3) // 4 * 4, (elem.num_face_nodes + 7) // 8 * 8
+        _SLOT_ORDERS[elem.order] = face_slot_order(elem.face_nodes, elem.order, npg, nfpk)
+    return _SLOT_ORDERS[elem.order]
 
 
 def geometry_words(geometry: GeometricFactors) -> np.ndarray:
@@ -102,7 +117,7 @@ class B200MaxwellOperator:
     def __init__(self, elem: ReferenceElement, material: Material, geo_words: np.ndarray,
                  det_j: np.ndarray, maps: FaceMaps, *, num_ghost: int = 0,
                  dtype: torch.dtype = torch.float32, device=None, path: str = "auto",
-                 order: np.ndarray | None = None):
+                 order: np.ndarray | None = None, face_slots: bool | None = None):
         if dtype not in _DTYPES:
             raise ValueError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
         if not torch.cuda.is_available():
@@ -128,12 +143,32 @@ class B200MaxwellOperator:
             if not np.array_equal(np.sort(order), np.arange(self.num_elements)):
                 raise ValueError("order must be a permutation of the owned elements")
             geo_words, det_j, maps = geo_words[order], det_j[order], permute_maps(maps, order)
+        # face-node slot order (ordering.face_slot_order): the nodes of each face are renumbered so
+        # that the tensor-core flux pass's shared-memory trace loads spread over the banks; fmask,
+        # the code table and the LIFT columns are permuted together, surface_flux maps back
+        if path not in _capi.PATHS:
+            raise ValueError(f"path must be one of {sorted(_capi.PATHS)}, got {path!r}")
+        if face_slots is None:
+            face_slots = bool(lay.tc_supported) and path != "simt"
+        lift = elem.lift
+        self._slot_inv = None
+        if face_slots:
+            from .ordering import permute_face_slots
+
+            perm = _face_slot_order(elem)
+            maps = permute_face_slots(maps, perm)
+            n_fp = elem.num_face_nodes
+            cols = (np.arange(NUM_FACES)[:, None] * n_fp + perm).reshape(-1)
+            lift = elem.lift[:, cols]
+            inv = np.empty_like(cols)
+            inv[cols] = np.arange(len(cols))
+            self._slot_inv = torch.as_tensor(inv, device=self.device)
 
         def dev(a, dt=dtype):
             return torch.as_tensor(np.ascontiguousarray(a)).to(device=self.device, dtype=dt)
 
         self._diff = dev(np.stack([pack_chunks(elem.diff[m], lay.diff_chunks, lay.vec) for m in range(3)]))
-        self._lift = dev(pack_chunks(elem.lift, lay.lift_chunks, lay.vec))
+        self._lift = dev(pack_chunks(lift, lay.lift_chunks, lay.vec))
         self._mass = dev(pack_chunks(elem.mass, lay.diff_chunks, lay.vec))
         self._geo = dev(geo_words)
         self._det = dev(det_j)
@@ -148,15 +183,13 @@ class B200MaxwellOperator:
             inv[order] = np.arange(len(order))
             self._inv = torch.as_tensor(inv, device=self.device)
         self._code = dev(cod, torch.int32)
-        self._fmask = dev(np.asarray(elem.face_nodes, dtype=np.uint8), torch.uint8)
+        self._fmask = dev(np.asarray(maps.face_nodes, dtype=np.uint8), torch.uint8)
         table = maps.code_table if len(maps.code_table) else np.zeros((1, elem.num_face_nodes), np.uint8)
         self._ptab = dev(table, torch.uint8)
         self._num_codes = int(len(maps.code_table))
-        if path not in _capi.PATHS:
-            raise ValueError(f"path must be one of {sorted(_capi.PATHS)}, got {path!r}")
         self._tc = None
         if lay.tc_supported and path != "simt":
-            self._tc = dev(tc_operand(elem, lay), torch.float32)
+            self._tc = dev(tc_operand(elem, lay, lift), torch.float32)
 
         desc = _capi.Desc(
             order=elem.order, dtype=self._dt_code, num_elements=self.num_elements,
@@ -354,6 +387,8 @@ class B200MaxwellOperator:
         _capi.check(self._lib.dgm_surface(self._plan, u.data_ptr(), out.data_ptr(), 0, self.num_elements,
                                           self._stream()), "dgm_surface")
         out = out[:, : self.num_elements]
+        if self._slot_inv is not None:
+            out = out.index_select(2, self._slot_inv)  # natural face-node order
         return out if self._inv is None else out.index_select(1, self._inv)  # natural numbering
 
     def rhs(self, state):
@@ -477,13 +512,16 @@ class B200MaxwellOperator:
 def build_b200_operator(mesh: Mesh, elem: ReferenceElement, material: Material = VACUUM,
                         connectivity: FaceConnectivity | None = None, *,
                         dtype: torch.dtype = torch.float32, device=None, path: str = "auto",
-                        reorder: bool | str | None = None) -> B200MaxwellOperator:
+                        reorder: bool | str | None = None,
+                        face_slots: bool | None = None) -> B200MaxwellOperator:
     """Drop-in for build_reference_operator (oracle.py:97-141) on one B200.
 
     ``reorder=True`` numbers the elements internally in 2x2-cell columns of their centroids
     (``"morton"``: along a Morton curve; paper_0901_1024_b200/ordering.py); the natural-order API
     is unchanged.  Default (None): on for 2 <= N <= 8 (C3 fp32 1.63 -> 1.54 ms per stage, fp64
     and N = 7, 8 0.4-1.3 % faster; N = 1 and N = 9 keep the reference numbering).
+    ``face_slots`` (default: whenever the tensor path is available) renumbers the nodes inside
+    each face for conflict-free shared-memory flux loads (ordering.face_slot_order).
     """
     if reorder is None:
         reorder = 2 <= elem.order <= 8
@@ -498,7 +536,7 @@ def build_b200_operator(mesh: Mesh, elem: ReferenceElement, material: Material =
         fn = ordering.morton_order if reorder == "morton" else ordering.column_order
         order = fn(mesh.vertices, mesh.elements)
     op = B200MaxwellOperator(elem, material, geometry_words(geometry), geometry.det_jacobians, maps,
-                             dtype=dtype, device=device, path=path, order=order)
+                             dtype=dtype, device=device, path=path, order=order, face_slots=face_slots)
     op.mesh = mesh
     op.connectivity = connectivity
     op.geometry = geometry

@@ -76,3 +76,95 @@ def permute_maps(maps: FaceMaps, order: np.ndarray) -> FaceMaps:
     nbr = np.where(nb < k, inv[np.minimum(nb, k - 1)], nb).astype(np.int32)
     return FaceMaps(num_nodes=maps.num_nodes, face_nodes=maps.face_nodes, neighbors=nbr,
                     codes=maps.codes[order].copy(), code_table=maps.code_table)
+
+
+# ----------------------------------------------------------------------------------------------
+# Face-node slot order of the tensor-core flux pass (dgm_tc.cuh flux_pass)
+# ----------------------------------------------------------------------------------------------
+
+def _flux_lane_groups(order: int, np_stride: int, nfp: int, nfpk: int):
+    """(rows, slots) of the 32 lanes of every (warp, node j) shared load of the flux pass.
+
+    Mirrors dgm_tc.cuh: TcCfg<N>::TE elements per CTA, FB = 4 face nodes per work unit,
+    unit = tid -> row = unit / NBF, slot = (unit % NBF) * FB + j; the owned-row trace load of a
+    lane reads s_u[row * NPG + fmask[face][slot]] (pad slots read slot 0).
+    """
+    te = 64 if order <= 6 else (32 if order <= 8 else 16)
+    fb, nbf = 4, nfpk // 4
+    rows, slots = [], []
+    for w in range((te * nbf + 31) // 32):
+        u = np.arange(w * 32, w * 32 + 32)
+        u = u[u // nbf < te]
+        for j in range(fb):
+            r = np.zeros(32, np.int64)
+            s = np.full(32, -1, np.int64)
+            r[: len(u)], s[: len(u)] = u // nbf, (u % nbf) * fb + j
+            rows.append(r)
+            slots.append(s)
+    rows, slots = np.array(rows), np.array(slots)
+    live = slots >= 0
+    slots = np.where((slots >= nfp) | ~live, 0, slots)  # pad slots read node slot 0
+    return rows * np_stride, slots, live
+
+
+def _bank_cost(nodes: np.ndarray, base: np.ndarray, slots: np.ndarray, live: np.ndarray) -> int:
+    """Sum over load groups of the max lanes per shared bank (wavefronts per load)."""
+    g = len(base)
+    banks = (base + nodes[slots]) % 32 + 32 * np.arange(g)[:, None]
+    counts = np.bincount(banks[live], minlength=32 * g).reshape(g, 32)
+    return int(counts.max(axis=1).sum())
+
+
+def face_slot_order(face_nodes: np.ndarray, order: int, np_stride: int, nfpk: int) -> np.ndarray:
+    """(4, Nfp) permutation: slot i of face f holds face node perm[f, i].
+
+    The order of the nodes inside a face is free (fmask, the code table and the LIFT columns are
+    permuted together), so it is chosen to spread the flux pass's owned-row trace loads over the
+    32 shared-memory banks: a deterministic pairwise-swap descent on the lane model above
+    (e.g. N=4: 2.0 -> 1.0..1.25 wavefronts per load).
+    """
+    face_nodes = np.asarray(face_nodes, dtype=np.int64)
+    nf, nfp = face_nodes.shape
+    base, slots, live = _flux_lane_groups(order, np_stride, nfp, nfpk)
+    perms = np.empty((nf, nfp), dtype=np.int64)
+    for f in range(nf):
+        perm = np.arange(nfp)
+        cur = _bank_cost(face_nodes[f][perm], base, slots, live)
+        improved = True
+        while improved:
+            improved = False
+            for a in range(nfp):
+                for b in range(a + 1, nfp):
+                    perm[[a, b]] = perm[[b, a]]
+                    c = _bank_cost(face_nodes[f][perm], base, slots, live)
+                    if c < cur:
+                        cur, improved = c, True
+                    else:
+                        perm[[a, b]] = perm[[b, a]]
+        perms[f] = perm
+    return perms
+
+
+def permute_face_slots(maps: FaceMaps, perm: np.ndarray) -> FaceMaps:
+    """FaceMaps whose face node i of face f is the natural face node perm[f, i].
+
+    Code-table rows are per (own face, code) after the permutation, so codes are re-issued.
+    """
+    nf = perm.shape[0]
+    face_nodes = np.take_along_axis(np.asarray(maps.face_nodes, dtype=np.int64), perm, axis=1)
+    codes = np.asarray(maps.codes)
+    new_codes = np.full_like(codes, -1)
+    rows: dict = {}
+    table = []
+    for f in range(nf):
+        col = codes[:, f]
+        for c in np.unique(col[col >= 0]):
+            row = np.asarray(maps.code_table[c])[perm[f]].astype(np.uint8)
+            key = row.tobytes()
+            if key not in rows:
+                rows[key] = len(table)
+                table.append(row)
+            new_codes[col == c, f] = rows[key]
+    code_table = np.array(table, dtype=np.uint8).reshape(len(table), perm.shape[1])
+    return FaceMaps(num_nodes=maps.num_nodes, face_nodes=face_nodes, neighbors=maps.neighbors,
+                    codes=new_codes, code_table=code_table)

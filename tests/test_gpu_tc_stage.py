@@ -112,3 +112,25 @@ def test_locality_reordered_operator_matches_oracle(n):
     plain.advance(b, 1e-3, 3, use_graph=False)
     assert rel_l2(op.from_padded(a).cpu().numpy(), plain.from_padded(b).cpu().numpy()) < 1e-5
     assert abs(op.field_energy(a) - plain.field_energy(b)) <= 1e-5 * plain.field_energy(b)
+
+
+@pytest.mark.parametrize("n", [3, 4, 6, 9])
+def test_face_slot_order_is_invisible(n):
+    """face_slots=True (bank-spread node order inside each face) vs the natural order: same RHS,
+    same natural-order surface flux, same steps; also on the fp64 SIMT path.  The natural plan is
+    created second with fewer codes (less smem): it must not shrink the first plan's smem limit."""
+    mesh = _jittered(80 + n, (4, 3, 3))
+    elem = build_reference_element(n)
+    ora = build_oracle_operator(mesh, elem)
+    state = np.random.default_rng(n).normal(size=(6, mesh.num_elements, elem.num_nodes))
+    slot = build_b200_operator(mesh, elem, path="tensor", face_slots=True)
+    nat = build_b200_operator(mesh, elem, path="tensor", face_slots=False)
+    assert slot._slot_inv is not None and nat._slot_inv is None
+    assert rel_l2(slot.rhs(state), ora.rhs(state)) < 1e-5
+    sa, sb = slot.to_padded(state), nat.to_padded(state)
+    assert rel_l2(slot.surface_flux(sa).cpu().numpy(), nat.surface_flux(sb).cpu().numpy()) < 1e-6
+    slot.advance(sa, 1e-3, 3, use_graph=False)
+    nat.advance(sb, 1e-3, 3, use_graph=False)
+    assert rel_l2(slot.from_padded(sa).cpu().numpy(), nat.from_padded(sb).cpu().numpy()) < 1e-5
+    f64 = build_b200_operator(mesh, elem, dtype=torch.float64, face_slots=True)
+    assert rel_l2(f64.rhs(state), ora.rhs(state)) < 1e-12

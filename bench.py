@@ -289,7 +289,7 @@ def run_b200(args) -> None:
     fp32_peak_tf = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
 
     # ---- end-to-end through the public API with host buffers ----
-    # Every e2e step uploads its own input (the f64 natural state, pinned host memory), packs it,
+    # Every e2e step uploads its own input (the natural state in the e2e dtype, pinned host memory), packs it,
     # runs one LSRK4 step, unpacks and downloads the new state and the energy scalar.  The steps are
     # independent, so on one GPU they rotate over four CUDA streams with separate device
     # buffers / workspaces: one step's D2H overlaps the next step's H2D (PCIe is full duplex) and

@@ -289,48 +289,71 @@ def run_b200(args) -> None:
     fp32_peak_tf = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
 
     # ---- end-to-end through the public API with host buffers ----
-    # Every e2e step uploads its own input (the natural state in the e2e dtype, pinned host memory), packs it,
-    # runs one LSRK4 step, unpacks and downloads the new state and the energy scalar.  The steps are
-    # independent, so on one GPU they rotate over four CUDA streams with separate device
-    # buffers / workspaces: one step's D2H overlaps the next step's H2D (PCIe is full duplex) and
-    # compute.  Every byte counted below still crosses PCIe inside the timed region.
+    # Every e2e step uploads its own input (the natural state in the e2e dtype, pinned host memory),
+    # packs it, runs one LSRK4 step, unpacks and downloads the new state and the energy scalar.  The
+    # steps are independent and pipelined over three streams: uploads in order on an H2D stream,
+    # pack/step/unpack on the compute stream, downloads in order on a D2H stream, with events
+    # recycling `--e2e-slots` device input buffers, so both copy engines stream back to back (PCIe
+    # is full duplex) while the GPU computes.  Every byte counted below crosses PCIe inside the
+    # timed region.
     e2e_steps = max(1, args.steps if args.e2e_steps is None else min(args.steps, args.e2e_steps))
     # natural host state in the e2e dtype (default: the compute dtype -- an fp32 user keeps fp32 host
     # buffers; --e2e-dtype f64 keeps the reference's float64 and doubles the PCIe bytes)
     e2e_dtype = {"f32": torch.float32, "f64": torch.float64}[args.e2e_dtype or args.dtype]
     host_in = torch.from_numpy(np.ascontiguousarray(u0_host)).to(e2e_dtype).pin_memory()
-    nstreams = args.e2e_streams if world == 1 else 1
-    host_out = [torch.empty_like(host_in).pin_memory() for _ in range(nstreams)]
-    e_host = [torch.empty(1, dtype=torch.float64).pin_memory() for _ in range(nstreams)]
+    nslots = max(2, args.e2e_slots)
+    host_out = [torch.empty_like(host_in).pin_memory() for _ in range(nslots)]
+    e_host = [torch.empty(1, dtype=torch.float64).pin_memory() for _ in range(nslots)]
     h2d = host_in.numel() * host_in.element_size()
     d2h = host_out[0].numel() * host_out[0].element_size() + 8
-    streams = [torch.cuda.Stream(dev) for _ in range(nstreams)] if world == 1 else [stream]
-    ues = [op.empty_state() for _ in range(nstreams)]
-    works = [op.workspace() for _ in range(nstreams)] if world == 1 else [None]
+    h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    dev_in = [torch.empty(host_in.shape, dtype=e2e_dtype, device=dev) for _ in range(nslots)]
+    ue = op.empty_state()  # one compute stream: the state buffer is reused in stream order
+    in_ready = [torch.cuda.Event() for _ in range(nslots)]   # H2D into dev_in[j] done
+    in_free = [torch.cuda.Event() for _ in range(nslots)]    # dev_in[j] packed (reusable)
+    out_ready = [torch.cuda.Event() for _ in range(nslots)]  # slot j's result unpacked
+    out_free = [torch.cuda.Event() for _ in range(nslots)]   # slot j's result downloaded
+    used = [False] * nslots
 
-    def e2e_step(j):
-        with torch.cuda.stream(streams[j]):
-            op.to_padded(host_in.to(dev, non_blocking=True), out=ues[j])   # H2D + pack (f64 natural -> padded)
-            if world == 1:
-                op.advance(ues[j], dt, 1, use_graph=False, workspace=works[j])  # 5 fused stage launches
-            else:
-                advance(ues[j], 1)
-            host_out[j].copy_(op.from_padded(ues[j], e2e_dtype), non_blocking=True)  # unpack + D2H of the new state
-            e_host[j].copy_(op.mass_norm(ues[j], 1.0, 1.0), non_blocking=True)  # per-step energy scalar
+    def e2e_step(i):
+        j = i % nslots
+        with torch.cuda.stream(h2d_s):
+            if used[j]:
+                h2d_s.wait_event(in_free[j])
+            dev_in[j].copy_(host_in, non_blocking=True)                     # H2D
+            in_ready[j].record(h2d_s)
+        with torch.cuda.stream(stream):
+            stream.wait_event(in_ready[j])
+            op.to_padded(dev_in[j], out=ue)                                 # pack (natural -> padded)
+            in_free[j].record(stream)
+            advance(ue, 1)                                                  # 5 fused stage launches
+            if used[j]:
+                stream.wait_event(out_free[j])  # bounds the results in flight to nslots
+            nat = op.from_padded(ue, e2e_dtype)                             # unpack
+            energy_dev = op.mass_norm(ue, 1.0, 1.0)                         # per-step energy scalar
+            nat.record_stream(d2h_s)
+            energy_dev.record_stream(d2h_s)
+            out_ready[j].record(stream)
+        with torch.cuda.stream(d2h_s):
+            d2h_s.wait_event(out_ready[j])
+            host_out[j].copy_(nat, non_blocking=True)                       # D2H of the new state
+            e_host[j].copy_(energy_dev, non_blocking=True)
+            out_free[j].record(d2h_s)
+        used[j] = True
 
-    for j in range(nstreams):  # warm-up (allocations, first launches)
+    for j in range(nslots):  # warm-up (allocations, first launches)
         e2e_step(j)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record(stream)
-    for st in streams:
-        st.wait_stream(stream)
+    h2d_s.wait_stream(stream)
+    d2h_s.wait_stream(stream)
     for i in range(e2e_steps):
-        e2e_step(i % nstreams)
-    for st in streams:
-        stream.wait_stream(st)
+        e2e_step(i)
+    stream.wait_stream(h2d_s)
+    stream.wait_stream(d2h_s)
     e_stop.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -385,11 +408,11 @@ def run_b200(args) -> None:
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_gflops, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,
-                "streams": nstreams,
+                "slots": nslots,
                 "host_dtype": str(e2e_dtype).replace("torch.", ""),
                 "path": "per step: pinned natural state H2D -> op.to_padded -> op.advance(1 LSRK4 step) -> "
-                        "op.from_padded -> pinned host D2H, + energy scalar D2H; independent steps alternate "
-                        "over %d CUDA stream(s)" % nstreams},
+                        "op.from_padded -> pinned host D2H, + energy scalar D2H; pipelined over an H2D, a "
+                        "compute and a D2H stream with %d input slots" % nslots},
         "gpu_launches": launches,
         "clocks": clk,
         "energy_after": energy,
@@ -409,8 +432,8 @@ def main(argv=None) -> None:
     ap.add_argument("--cells", type=int, nargs=3, default=list(CELLS))
     ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
     ap.add_argument("--e2e-steps", type=int, default=None, help="e2e steps (default: --steps)")
-    ap.add_argument("--e2e-streams", type=int, default=4,
-                    help="CUDA streams the independent e2e steps rotate over (one GPU)")
+    ap.add_argument("--e2e-slots", type=int, default=4,
+                    help="device input buffers of the e2e pipeline (H2D runs up to this many steps ahead)")
     ap.add_argument("--element-order", choices=("auto", "natural", "morton", "columns"), default="auto",
                     help="internal element numbering (ordering.py); auto = Morton where it pays")
     ap.add_argument("--face-slots", choices=("auto", "natural"), default="auto",

@@ -35,12 +35,45 @@ CELLS = (55, 55, 55)
 CPU_SAMPLE_CELLS = (6, 6, 7)
 
 
+def _flatten(d, prefix=""):
+    for key, val in (d.items() if isinstance(d, dict) else []):
+        path = f"{prefix}.{key}" if prefix else str(key)
+        if isinstance(val, dict):
+            yield from _flatten(val, path)
+        elif isinstance(val, (int, float)) and not isinstance(val, bool):
+            yield path, float(val)
+
+
 def _peaks() -> dict:
+    """HBM peak for the roofline: MEASURED_PEAKS.json (driver-written) else the B200_PROFILING.md fallback.
+
+    The file's key names are not fixed here, so its numeric entries are searched for an HBM / DRAM
+    / copy bandwidth; the sustained figure is preferred (the stage kernel runs inside a long step),
+    then burst, then any; values below 100 are taken as TB/s.
+    """
+    fallback = {"hbm_gbs": 6650.0, "source": "fallback 6.65 TB/s (B200_PROFILING.md)", "_fallback": True}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f)
-    except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+            data = json.load(f)
+    except (OSError, ValueError):
+        return fallback
+    cands = [(k, v) for k, v in _flatten(data)
+             if any(t in k.lower() for t in ("hbm", "dram", "copy", "mem_bw", "bandwidth")) and v > 0
+             and not any(t in k.lower() for t in ("tflop", "flops", "mhz", "clock"))]
+    if not cands:
+        return fallback
+
+    def rank(item):
+        k = item[0].lower()
+        return (0 if "sustain" in k else 1 if "burst" in k else 2, k)
+
+    key, val = sorted(cands, key=rank)[0]
+    gbs = val * 1000.0 if val < 100.0 else val
+    out = {"hbm_gbs": gbs, "source": f"MEASURED_PEAKS.json {key}"}
+    for k, v in _flatten(data):
+        if "mhz" in k.lower() and "max" in k.lower():
+            out["sm_max_mhz"] = v
+    return out
 
 
 def _ncu_summary() -> dict:
@@ -401,8 +434,7 @@ def run_b200(args) -> None:
                                 f"dgm::stage_kernel<{args.order},{'float' if word == 4 else 'double'},1>"),
                      "path": op.path,
                      "launch_us": launch_s * 1e6,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "_fallback" not in peaks
-                     else "fallback 6.65 TB/s (B200_PROFILING.md)",
+                     "peak_source": peaks["source"],
                      "fp32_simt_frac": f_alg * k / launch_s / 1e12 / fp32_peak_tf,
                      "fp32_simt_peak_tflops": fp32_peak_tf},
         "cpu_baseline": cpu,

@@ -7,6 +7,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import bench  # noqa: E402
+import pytest  # noqa: E402
 
 
 def _line(sm, smax=1965, power_cap="Not Active", thermal="Not Active"):
@@ -37,3 +38,21 @@ def test_flop_and_byte_model_matches_survey_appendix_b():
 
     assert flops_per_element_stage(4) == 76410 and flops_per_element_stage(6) == 381864
     assert bytes_per_element_stage(4, 4) == 3496 and bytes_per_element_stage(9, 4) == 21256
+
+
+@pytest.mark.parametrize("data,want,key", [
+    ({"hbm_gbs": 6535.2, "bf16_tflops": 1500.0}, 6535.2, "hbm_gbs"),
+    ({"hbm": {"copy_gbs_burst": 6800.0, "copy_gbs_sustained": 6535.0}}, 6535.0, "hbm.copy_gbs_sustained"),
+    ({"dram_tbs": 6.5}, 6500.0, "dram_tbs"),
+])
+def test_measured_peaks_parsing(tmp_path, monkeypatch, data, want, key):
+    """bench._peaks reads the driver-written MEASURED_PEAKS.json whatever its key layout."""
+    import json
+
+    import bench
+
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    assert bench._peaks()["_fallback"]
+    (tmp_path / "MEASURED_PEAKS.json").write_text(json.dumps(data))
+    got = bench._peaks()
+    assert got["hbm_gbs"] == pytest.approx(want) and got["source"].endswith(key)

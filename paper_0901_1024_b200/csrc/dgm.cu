@@ -318,9 +318,23 @@ int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, vo
         const int64_t tt = (e_end - e_begin + TC::TE - 1) / TC::TE;
         targs.num_tiles = (int)tt;
         targs.wave = TC::CTAS * plan->num_sms;
-        dgm::tc_stage_kernel<N, MODE><<<(unsigned)tt, TC::THREADS, plan->tc_smem, static_cast<cudaStream_t>(stream)>>>(
-            targs);
-        return cuda_check(cudaGetLastError(), "tc_stage_kernel launch");
+        // programmatic dependent launch: the grid may start during its predecessor's tail; the
+        // kernel runs its state-independent prologue, then griddepcontrol.wait (dgm_tc.cuh)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)tt);
+        cfg.blockDim = dim3(TC::THREADS);
+        cfg.dynamicSmemBytes = plan->tc_smem;
+        cfg.stream = static_cast<cudaStream_t>(stream);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+#ifdef DGM_NO_PDL
+        attr[0].val.programmaticStreamSerializationAllowed = 0;
+#else
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+#endif
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cuda_check(cudaLaunchKernelEx(&cfg, dgm::tc_stage_kernel<N, MODE>, targs), "tc_stage_kernel launch");
       }
     }
     const int64_t tiles = (e_end - e_begin + C::TE - 1) / C::TE;

@@ -252,6 +252,9 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
   // instead of all hitting the same lines at once.  Face steps stay contiguous.
   const int rot = (int)(blockIdx.x % (unsigned)(KV / 8));
 
+  // PDL: the next stage's grid may be scheduled once every CTA of this one has started (it then runs
+  // its state-independent prologue on the SMs freed by this grid's tail and waits in griddep_wait)
+  griddep_launch();
   if (warp == 0) tmem_alloc(s_tmem, T::TMEM_COLS);
   if (tid == PROD) {
     for (int i = 0; i < AST; ++i) {
@@ -297,6 +300,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       bulk_g2s(s_geo, a.geo + e0 * GEO_WORDS, geobytes, load_full);
       bulk_g2s(s_nbr, a.nbr + e0 * 4, conbytes, load_full);
       bulk_g2s(s_code, a.code + e0 * 4, conbytes, load_full);
+      griddep_wait();  // everything above is constant; the state below is the previous stage's output
       for (int f = 0; f < 6; ++f)
         bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowbytes, load_full);
       if (MODE == MODE_LSRK && !a.a_zero && KS <= NBS) prefetch_res();
@@ -366,6 +370,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     // MAP 0: one material factor per thread (folded into prx); MAP 1: per component
     const float inv_m = T::MAP == 0 ? (h == 0 ? a.inv_eps : a.inv_mu) : 1.f;
     if (tid == 0) TC_TRACE(0, 1);  // start
+    griddep_wait();  // before any global access to the state / residual (neighbour gathers, epilogue)
     mbar_wait(load_full, 0);
     if (tid == 0) TC_TRACE(0, 2);  // rows landed
     // warm L2 with the rows of every face neighbour outside the tile (read by the face K-steps);

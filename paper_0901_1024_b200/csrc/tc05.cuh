@@ -149,6 +149,12 @@ __device__ __forceinline__ void mbar_wait(void* mbar, uint32_t parity) {
 }
 #endif
 
+// Programmatic dependent launch (PDL): a grid launched with programmatic stream serialization may
+// start while its predecessor on the stream is still running; griddep_wait() blocks until that grid
+// has completed and its memory is visible, griddep_launch() lets the successor start early.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operands).
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

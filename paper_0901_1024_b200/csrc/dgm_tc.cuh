@@ -372,6 +372,13 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     if (tid == 0) TC_TRACE(0, 1);  // start
     griddep_wait();  // before any global access to the state / residual (neighbour gathers, epilogue)
     mbar_wait(load_full, 0);
+    if (nv < TE) {  // partial tile: zero the unused rows once, so no per-value row masking is needed
+      for (int i = tid; i < 6 * (TE - nv) * NPG; i += PROD) {
+        const int f = i / ((TE - nv) * NPG), rem = i - f * (TE - nv) * NPG;
+        s_u[(f * TE + nv) * NPG + rem] = 0.f;
+      }
+      named_sync(1, PROD);
+    }
     if (tid == 0) TC_TRACE(0, 2);  // rows landed
     // warm L2 with the rows of every face neighbour outside the tile (read by the face K-steps);
     // issued LEAD K-steps before this CTA's first face step (-1: at tile start);
@@ -440,7 +447,10 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         const int k = k0 + CW * kh;
         if (k < 3 * NPK) {
           const int mu = k / NPK, j0 = k - mu * NPK;
-          const float p0 = prx[mu * 3 + 0], p1 = prx[mu * 3 + 1], p2 = prx[mu * 3 + 2];
+          // register selects, not prx[mu * 3 + .] (a dynamic index puts prx in local memory)
+          const float p0 = mu == 0 ? prx[0] : (mu == 1 ? prx[3] : prx[6]);
+          const float p1 = mu == 0 ? prx[1] : (mu == 1 ? prx[4] : prx[7]);
+          const float p2 = mu == 0 ? prx[2] : (mu == 1 ? prx[5] : prx[8]);
           const int fb = h == 0 ? 3 : 0;  // E comps read H fields and vice versa
           float xs[CW], ys[CW], zs[CW];
           lds_vec<CW>(s_u + ((fb + 0) * TE + row) * NPG + j0, xs);
@@ -561,7 +571,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #pragma unroll
         for (int t = 0; t < MT; ++t)
 #pragma unroll
-          for (int q = 0; q < T::CW; ++q) split_tf32(row_ok ? vcur[j][t][q] : 0.f, hi[t][q], lo[t][q]);
+          for (int q = 0; q < T::CW; ++q) split_tf32(vcur[j][t][q], hi[t][q], lo[t][q]);  // dead rows are 0
         if (j == 0) {
           mbar_wait(&empty[slot], ((i / AST) & 1) ^ 1);
           if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free

@@ -409,6 +409,23 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     float prx[9];  // geometric factors of the owned row, pre-scaled by 1/eps or 1/mu
 #pragma unroll
     for (int q = 0; q < 9; ++q) prx[q] = row_ok ? s_geo[row * GEO_WORDS + q] * inv_m : 0.f;
+    // MAP 1/2: the curl factors (dr_mu/dx_c1, dr_mu/dx_c2) / eps or mu of each M-tile's component,
+    // per mu, so the K loop selects registers instead of indexing prx with a runtime component
+    float pa3[MT][3], pb3[MT][3];
+    if constexpr (T::MAP != 0) {
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        const int c = T::comp_of(t, quad, lane);
+        const int cc = c % 3, c1 = (cc + 1) % 3, c2 = (cc + 2) % 3;
+        const float m = c < 3 ? a.inv_eps : -a.inv_mu;
+#pragma unroll
+        for (int mu = 0; mu < 3; ++mu) {
+          const bool ok = row_ok && c < 6;
+          pa3[t][mu] = ok ? s_geo[row * GEO_WORDS + mu * 3 + c1] * m : 0.f;
+          pb3[t][mu] = ok ? s_geo[row * GEO_WORDS + mu * 3 + c2] * m : 0.f;
+        }
+      }
+    }
 
     // A values of K-step s for this thread's row (4 columns x 3 M-tiles), unsplit
     auto a_values = [&](int s, int kh, float (&v)[MT][T::CW]) {
@@ -427,8 +444,8 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
             const int mu = k / NPK, j0 = k - mu * NPK;
             const int cc = c % 3, c1 = (cc + 1) % 3, c2 = (cc + 2) % 3;
             const int fb = c < 3 ? 3 : 0;  // E comps read H fields and vice versa
-            const float m = c < 3 ? a.inv_eps : -a.inv_mu;
-            const float pa = prx[mu * 3 + c1] * m, pb = prx[mu * 3 + c2] * m;
+            const float pa = mu == 0 ? pa3[t][0] : (mu == 1 ? pa3[t][1] : pa3[t][2]);
+            const float pb = mu == 0 ? pb3[t][0] : (mu == 1 ? pb3[t][1] : pb3[t][2]);
             float xp[CW], yp[CW];
             lds_vec<CW>(s_u + ((fb + c2) * TE + row) * NPG + j0, xp);
             lds_vec<CW>(s_u + ((fb + c1) * TE + row) * NPG + j0, yp);

@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     const int row = T::row_of(quad, lane);   // element row of this TMEM lane
     const uint32_t lane_addr = static_cast<uint32_t>(quad * 32) << 16;
     // MAP 0: one material factor per thread (folded into prx); MAP 1: per component
-    const float inv_m = T::MAP == 0 ? (h == 0 ? a.inv_eps : a.inv_mu) : 1.f;
+    // (the sign of -(curl E) / mu is folded in, so both halves use the curl H formula below)
+    const float inv_m = T::MAP == 0 ? (h == 0 ? a.inv_eps : -a.inv_mu) : 1.f;
     if (tid == 0) TC_TRACE(0, 1);  // start
     griddep_wait();  // before any global access to the state / residual (neighbour gathers, epilogue)
     mbar_wait(load_full, 0);
@@ -474,16 +475,10 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
           lds_vec<CW>(s_u + ((fb + 1) * TE + row) * NPG + j0, ys);
           lds_vec<CW>(s_u + ((fb + 2) * TE + row) * NPG + j0, zs);
 #pragma unroll
-          for (int q = 0; q < CW; ++q) {
-            if (h == 0) {  // (curl H)_x,y,z
-              v[0][q] = p1 * zs[q] - p2 * ys[q];
-              v[1][q] = p2 * xs[q] - p0 * zs[q];
-              v[2][q] = p0 * ys[q] - p1 * xs[q];
-            } else {       // -(curl E)_x,y,z
-              v[0][q] = p2 * ys[q] - p1 * zs[q];
-              v[1][q] = p0 * zs[q] - p2 * xs[q];
-              v[2][q] = p1 * xs[q] - p0 * ys[q];
-            }
+          for (int q = 0; q < CW; ++q) {  // (curl H) / eps, or -(curl E) / mu via the sign in p
+            v[0][q] = p1 * zs[q] - p2 * ys[q];
+            v[1][q] = p2 * xs[q] - p0 * zs[q];
+            v[2][q] = p0 * ys[q] - p1 * xs[q];
           }
         } else if (k >= KV) {
           const int node = (k - KV) % NFPK;

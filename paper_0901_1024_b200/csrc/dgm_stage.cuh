@@ -118,24 +118,31 @@ struct StageArgs {
 enum Mode { MODE_RHS = 0, MODE_LSRK = 1, MODE_VOLUME = 2, MODE_SURFACE = 3 };
 
 // Upwind flux difference (maxwell.py:73-114) for a uniform material.
+// Upwind bracket numerators, before the 1/(2{Z}) and 1/(2{Y}) factors (maxwell.py:73-114):
+//   E: n x (Z+ [[H]] - n x [[E]]) = Z+ (n x [[H]]) + [[E]] - n (n . [[E]])
+//   H: n x (-Y+ [[E]] - n x [[H]]) = -Y+ (n x [[E]]) + [[H]] - n (n . [[H]])
+// (n x (n x v) = n (n . v) - v for the unit normal: 36 instead of 48 operations per node).
+template <typename T>
+__device__ __forceinline__ void upwind_num(const T* um, const T* up, T nx, T ny, T nz, T zp, T yp, T* out) {
+  const T dex = up[0] - um[0], dey = up[1] - um[1], dez = up[2] - um[2];
+  const T dhx = up[3] - um[3], dhy = up[4] - um[4], dhz = up[5] - um[5];
+  const T nde = nx * dex + ny * dey + nz * dez, ndh = nx * dhx + ny * dhy + nz * dhz;
+  out[0] = zp * (ny * dhz - nz * dhy) + (dex - nx * nde);
+  out[1] = zp * (nz * dhx - nx * dhz) + (dey - ny * nde);
+  out[2] = zp * (nx * dhy - ny * dhx) + (dez - nz * nde);
+  out[3] = (dhx - nx * ndh) - yp * (ny * dez - nz * dey);
+  out[4] = (dhy - ny * ndh) - yp * (nz * dex - nx * dez);
+  out[5] = (dhz - nz * ndh) - yp * (nx * dey - ny * dex);
+}
+
 template <typename T>
 __device__ __forceinline__ void upwind(const T* um, const T* up, T nx, T ny, T nz,
                                        const StageArgs<T>& a, T* out) {
-  const T dex = up[0] - um[0], dey = up[1] - um[1], dez = up[2] - um[2];
-  const T dhx = up[3] - um[3], dhy = up[4] - um[4], dhz = up[5] - um[5];
-  // n x [[E]], n x [[H]]
-  const T cex = ny * dez - nz * dey, cey = nz * dex - nx * dez, cez = nx * dey - ny * dex;
-  const T chx = ny * dhz - nz * dhy, chy = nz * dhx - nx * dhz, chz = nx * dhy - ny * dhx;
-  // E part: n x (Z+ [[H]] - n x [[E]]) / (2{Z})
-  const T ax = a.zp * dhx - cex, ay = a.zp * dhy - cey, az = a.zp * dhz - cez;
-  out[0] = (ny * az - nz * ay) * a.inv_2z;
-  out[1] = (nz * ax - nx * az) * a.inv_2z;
-  out[2] = (nx * ay - ny * ax) * a.inv_2z;
-  // H part: n x (-Y+ [[E]] - n x [[H]]) / (2{Y})
-  const T bx = -a.yp * dex - chx, by = -a.yp * dey - chy, bz = -a.yp * dez - chz;
-  out[3] = (ny * bz - nz * by) * a.inv_2y;
-  out[4] = (nz * bx - nx * bz) * a.inv_2y;
-  out[5] = (nx * by - ny * bx) * a.inv_2y;
+  upwind_num(um, up, nx, ny, nz, a.zp, a.yp, out);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out[c] *= a.inv_2z;
+#pragma unroll
+  for (int c = 3; c < 6; ++c) out[c] *= a.inv_2y;
 }
 
 template <int N, typename T, int MODE>

@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
           const float* gk = s_geo + r * GEO_WORDS;
           const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
           const float sc = row_live ? gk[22 + face] * gk[9] : 0.f;
-          const float se = sc * a.inv_eps, sh = sc * a.inv_mu;
+          const float se = sc * a.inv_eps * a.inv_2z, sh = sc * a.inv_mu * a.inv_2y;  // upwind factors folded
           int im[FB], jn[FB];
 #pragma unroll
           for (int j = 0; j < FB; ++j) {
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
               up[j][5] = um[5] - 2.f * ndh * nz;
             }
             float out[6];
-            upwind(um, up[j], nx, ny, nz, a, out);
+            upwind_num(um, up[j], nx, ny, nz, a.zp, a.yp, out);
             const int node = n0 + j;
             const float kse = node < NFP ? se : 0.f, ksh = node < NFP ? sh : 0.f;
 #pragma unroll

@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         }
         named_sync(1, PROD);
     };
-    auto face_start = [&](int s) { return s * 8 >= KV && (s * 8 - KV) % NFPK == 0; };
+    auto face_start = [&](int s) { return s >= KV / 8 && (s - KV / 8) % (NFPK / 8) == 0; };
 
     // Software-pipelined K loop: the next step's A values are computed between this step's
     // tcgen05.st and its tcgen05.wait::st, hiding the TMEM store latency; a flux pass (two named
@@ -571,10 +571,16 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #endif
 #pragma unroll
     for (int j = 0; j < T::KH; ++j) a_values((0 + rot) % KS, kh_of(j), vcur[j]);
+    // slot = i % AST, its empty-barrier parity ((i / AST) & 1) ^ 1 and the K-step s = (i + rot) % KS:
+    // kept as incremental counters where registers allow (1 CTA/SM: N=6 -3.3 %, N=8 -4.8 %), recomputed
+    // per step at 2 CTAs/SM, where the three extra live registers spill at the 96-register cap (+5.6 %)
+    constexpr bool INC = T::CTAS == 1;
+    int slot_c = 0, s_c = rot;
+    uint32_t eph_c = 1;
     for (int i = 0; i < KS; ++i) {  // i: position in this CTA's K order, s: K-step
-      const int slot = i % AST;
-      const int s = (i + rot) % KS;
-      (void)s;                                  // (trace builds only)
+      const int slot = INC ? slot_c : i % AST;
+      const int s = INC ? s_c : (i + rot) % KS;
+      const uint32_t eph = INC ? eph_c : (((i / AST) & 1) ^ 1);
       if (tid == 0) TC_TRACE(0, 100 + 4 * s);  // step begin
       if (i == nbr_pf_i) nbr_prefetch();
 #pragma unroll
@@ -585,7 +591,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #pragma unroll
           for (int q = 0; q < T::CW; ++q) split_tf32(vcur[j][t][q], hi[t][q], lo[t][q]);  // dead rows are 0
         if (j == 0) {
-          mbar_wait(&empty[slot], ((i / AST) & 1) ^ 1);
+          mbar_wait(&empty[slot], eph);
           if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free
           fence_after_sync();
         }
@@ -605,7 +611,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         if (hi[0][0] == 12345.f && lo[0][3] == 1.f) s_stage[0] = 0.f;  // keep the values live
 #endif
       }
-      const int sn = (i + 1 + rot) % KS;
+      const int sn = INC ? (s + 1 == KS ? 0 : s + 1) : (i + 1 + rot) % KS;
       const bool has_next = i + 1 < KS;
 #ifdef DGM_EXP_NOFLUX
       const bool next_flux = false;
@@ -632,6 +638,10 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         for (int t = 0; t < MT; ++t)
 #pragma unroll
           for (int q = 0; q < T::CW; ++q) vcur[j][t][q] = vnext[j][t][q];
+      if constexpr (INC) {
+        s_c = sn;
+        if (++slot_c == AST) slot_c = 0, eph_c ^= 1u;
+      }
     }
 
     // ================= epilogue: accumulators -> LSRK update =================

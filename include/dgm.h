@@ -94,6 +94,12 @@ enum { DGM_PATH_AUTO = 0, DGM_PATH_SIMT = 1, DGM_PATH_TENSOR = 2 };
  *  face_nodes  : uint8[4][Nfp]            elem.face_nodes (refelem.py:387-394)
  *  code_table  : uint8[num_codes][Nfp]    vmap_plus rows minus neighbor*Np
  *                (oracle.py:116-123)
+ *                The order of the nodes inside a face is free: a caller may
+ *                permute face f's slots (face_nodes[f], the code_table rows
+ *                used on face f and LIFT columns f*Nfp..) consistently; the
+ *                surface output (dgm_surface) then follows the same slot order.
+ *                The Python layer does so to spread the tensor kernel's
+ *                shared-memory loads (ordering.face_slot_order).
  *  tc_operand  : float[tc_steps][2][2][tc_nb][4], the constant GEMM operand
  *                B[n][k]: D_mu[n][j] at k = mu*tc_npk + j, LIFT[n][f*Nfp + i]
  *                at k = tc_kv + f*tc_nfpk + i, zero elsewhere; split into a

@@ -669,8 +669,15 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       // quadrant warps holding the phase's components: TMEM lanes -> smem rows [which][row][NPG]
       // (MAP 0: M-tile t, all four quadrants; MAP 1: M-tile t/2, quadrants 2(t%2), 2(t%2)+1)
       // (MAP 2: the single M-tile, quadrant t: lanes 0-15 component 2t, 16-31 component 2t+1)
-      const bool mover = khalf == 0 && (T::MAP == 0 || (T::MAP == 1 ? (quad >> 1) == (t & 1) : quad == t));
-      if (mover) {
+      // EPI_SPLIT (N=6): every column group of those quadrants moves a share of the NB / 8 column
+      // chunks, up to four tcgen05.ld in flight per wait (N=6 -3.8 %); elsewhere the first column group
+      // moves all chunks, one load per wait (the split measured N=4 +1.0 %, N=5 +1.3 %, N=8 +0.7 %,
+      // N=9 +1.5 %)
+      constexpr bool EPI_SPLIT = N == 6 && T::MAP == 0;
+      const bool mover = (EPI_SPLIT || khalf == 0) &&
+                         (T::MAP == 0 || (T::MAP == 1 ? (quad >> 1) == (t & 1) : quad == t));
+      if constexpr (!EPI_SPLIT) {
+       if (mover) {
         const int tile = T::MAP == 0 ? t : (T::MAP == 1 ? t >> 1 : 0);
         const int slot = T::MAP == 0 ? h : (T::MAP == 1 ? (quad & 1) : (lane >> 4));
         float* dst = s_stage + (size_t)slot * TE * NPG + row * NPG;
@@ -689,6 +696,38 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
               o.z = (i + 2 < NP) ? r8[q + 2] : 0.f;
               o.w = (i + 3 < NP) ? r8[q + 3] : 0.f;
               *reinterpret_cast<float4*>(dst + i) = o;
+            }
+          }
+        }
+       }
+      } else if (mover) {
+        const int tile = T::MAP == 0 ? t : (T::MAP == 1 ? t >> 1 : 0);
+        const int slot = T::MAP == 0 ? h : (T::MAP == 1 ? (quad & 1) : (lane >> 4));
+        float* dst = s_stage + (size_t)slot * TE * NPG + row * NPG;
+        constexpr int NC = NB / 8, CPG = (NC + T::NQ - 1) / T::NQ;  // chunks, chunks per column group
+        const int cb = khalf * CPG;
+#pragma unroll
+        for (int b0 = 0; b0 < CPG; b0 += 4) {
+          float r8[4][8];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (b0 + k < CPG && cb + b0 + k < NC) tmem_ld8(tmem + lane_addr + tile * NB + (cb + b0 + k) * 8, r8[k]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (b0 + k < CPG && cb + b0 + k < NC) {
+#pragma unroll
+              for (int q = 0; q < 8; q += 4) {
+                const int i = (cb + b0 + k) * 8 + q;
+                if (i < NPG) {
+                  float4 o;
+                  o.x = (i + 0 < NP) ? r8[k][q + 0] : 0.f;
+                  o.y = (i + 1 < NP) ? r8[k][q + 1] : 0.f;
+                  o.z = (i + 2 < NP) ? r8[k][q + 2] : 0.f;
+                  o.w = (i + 3 < NP) ? r8[k][q + 3] : 0.f;
+                  *reinterpret_cast<float4*>(dst + i) = o;
+                }
+              }
             }
           }
         }

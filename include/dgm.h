@@ -25,6 +25,8 @@
  *  - dtype: DGM_F32 or DGM_F64 selects the arithmetic type of every real
  *    buffer of a plan.
  *  - Streams are cudaStream_t passed as void*; NULL = legacy default stream.
+ *    Calls taking a plan launch on the device the plan was created on,
+ *    whatever the calling thread's current device (restored on return).
  *  - Return value 0 = success, negative = error class; the message is in
  *    dgm_last_error() (thread-local), mirroring the reference's ValueError /
  *    RuntimeError split (mesh.py:42-49, assemble.py:107-108).
@@ -182,20 +184,40 @@ int dgm_surface(const dgm_plan* plan, const void* u, void* out,
  * field_energy = 0.5 * value with (wE,wH) = (eps,mu)   (maxwell.py:225-232);
  * l2_error^2 = value of (u - exact) with w = 1           (maxwell.py:211-222).
  * mass_packed has the LIFT-style packing: real[diff_chunks][Np][vec].
- * det_j is real[num_elements].
+ * det_j is real[num_elements].  partials is device scratch of
+ * dgm_mass_norm_partials(plan, e_end - e_begin) doubles: one partial per CTA,
+ * summed by a second one-CTA kernel in a fixed order, so the result is bitwise
+ * reproducible run to run (the reference's reruns are byte-identical,
+ * pkg/tests/test_cli.py:106-112).
  */
 int dgm_mass_norm(const dgm_plan* plan, const void* u, const void* mass_packed,
                   const void* det_j, double w_e, double w_h, double* out_f64,
-                  int64_t e_begin, int64_t e_end, void* stream);
+                  double* partials, int64_t e_begin, int64_t e_end, void* stream);
+int64_t dgm_mass_norm_partials(const dgm_plan* plan, int64_t count);
 
 /*
- * Natural (6, K, Np) float64  ->  padded (6, field_stride, np_stride) real,
- * zero padding (reference fields.py:24-35 to_padded), and back.
+ * face_states (oracle.py:50-58): u_minus[f][k][face][i] = u at vmap_minus,
+ * u_plus = u at vmap_plus, with the PEC mirror (maxwell.py:117-132) on walls;
+ * both real[6][num_elements][4][Nfp] in the NATURAL numbering.  elem_nat
+ * (int64[num_elements], NULL = identity) maps the plan's element slot s to the
+ * natural element id; node_nat (uint8[4][Nfp], NULL = identity) maps the
+ * plan's face slot q of face f to the natural face-node index.
  */
-int dgm_pack(int32_t order, int32_t dtype, const double* natural, void* padded,
-             int64_t num_elements, int64_t field_stride, void* stream);
-int dgm_unpack(int32_t order, int32_t dtype, const void* padded, double* natural,
-               int64_t num_elements, int64_t field_stride, void* stream);
+int dgm_face_states(const dgm_plan* plan, const void* u, const int64_t* elem_nat,
+                    const uint8_t* node_nat, void* u_minus, void* u_plus, void* stream);
+
+/*
+ * Natural (6, K, Np) float64 or float32 (natural_dtype)  <->  padded
+ * (6, field_stride, np_stride) real, zero padding (reference fields.py:24-35
+ * to_padded / from_padded), cast and element permutation in one pass:
+ * padded slot s holds natural element perm[s] (perm = NULL: identity).
+ */
+int dgm_pack(int32_t order, int32_t dtype, const void* natural, int32_t natural_dtype,
+             const int64_t* perm, void* padded, int64_t num_elements,
+             int64_t field_stride, void* stream);
+int dgm_unpack(int32_t order, int32_t dtype, const void* padded, const int64_t* perm,
+               void* natural, int32_t natural_dtype, int64_t num_elements,
+               int64_t field_stride, void* stream);
 
 /*
  * Multi-GPU halo helpers: gather whole element rows of the listed elements

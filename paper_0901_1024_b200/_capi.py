@@ -13,7 +13,7 @@ from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DGM_LIB") or os.path.join(_HERE, "libdgm.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 GEO_WORDS = 28
 
 DGM_F32, DGM_F64 = 0, 1
@@ -60,9 +60,11 @@ _SIGNATURES = {
     "dgm_lsrk_stage": ([_VP, _VP, _VP, _VP, _D, _D, _D, _I64, _I64, _VP], ctypes.c_int),
     "dgm_volume": ([_VP, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
     "dgm_surface": ([_VP, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
-    "dgm_mass_norm": ([_VP, _VP, _VP, _VP, _D, _D, _VP, _I64, _I64, _VP], ctypes.c_int),
-    "dgm_pack": ([ctypes.c_int32, ctypes.c_int32, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
-    "dgm_unpack": ([ctypes.c_int32, ctypes.c_int32, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
+    "dgm_mass_norm": ([_VP, _VP, _VP, _VP, _D, _D, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
+    "dgm_mass_norm_partials": ([_VP, _I64], ctypes.c_int64),
+    "dgm_face_states": ([_VP, _VP, _VP, _VP, _VP, _VP, _VP], ctypes.c_int),
+    "dgm_pack": ([ctypes.c_int32, ctypes.c_int32, _VP, ctypes.c_int32, _VP, _VP, _I64, _I64, _VP], ctypes.c_int),
+    "dgm_unpack": ([ctypes.c_int32, ctypes.c_int32, _VP, _VP, _VP, ctypes.c_int32, _I64, _I64, _VP], ctypes.c_int),
     "dgm_halo_pack": ([_VP, _VP, _VP, _I64, _VP, _VP], ctypes.c_int),
     "dgm_halo_unpack": ([_VP, _VP, _I64, _I64, _VP, _VP], ctypes.c_int),
 }

@@ -16,7 +16,7 @@
 #include "dgm_stage.cuh"
 #include "dgm_tc.cuh"
 
-#define DGM_ABI_VERSION 2
+#define DGM_ABI_VERSION 3
 
 namespace {
 
@@ -73,6 +73,29 @@ int dispatch(int order, int dtype, Fn&& fn) {
 #undef DGM_CASE
 }
 
+// Launches of a plan run on the device the plan was created on, whatever the caller's current device
+// (the stream passed in belongs to that device); the previous current device is restored.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// Calls fn(TN{}) for the natural-side real type.
+template <typename Fn>
+int natural_dispatch(int natural_dtype, Fn&& fn) {
+  if (natural_dtype == DGM_F64) return fn(double{});
+  if (natural_dtype == DGM_F32) return fn(float{});
+  return fail(DGM_ERR_UNSUPPORTED, "natural dtype %d not supported", natural_dtype);
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int grid_for(int64_t work, int threads) {
@@ -90,6 +113,7 @@ struct dgm_plan {
   int path;           // DGM_PATH_SIMT or DGM_PATH_TENSOR
   size_t tc_smem;     // dynamic smem of the tensor-core stage kernels
   int num_sms;
+  int device;         // CUDA device the plan was created on (DeviceGuard)
 };
 
 namespace {
@@ -243,6 +267,7 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
   p->path = path;
   p->tc_smem = tc_smem;
   p->num_sms = sms > 0 ? sms : 148;
+  p->device = dev;
   *out = p;
   return DGM_OK;
 }
@@ -278,6 +303,7 @@ int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, vo
     return fail(DGM_ERR_INVALID, "output pointer must be non-null and 16-byte aligned");
   }
   if (e_end == e_begin) return DGM_OK;
+  DeviceGuard guard(plan->device);
   return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
     constexpr int N = decltype(n)::value;
     using T = decltype(t);
@@ -366,29 +392,72 @@ int dgm_surface(const dgm_plan* plan, const void* u, void* out, int64_t e_begin,
 }
 
 int dgm_mass_norm(const dgm_plan* plan, const void* u, const void* mass_packed, const void* det_j, double w_e,
-                  double w_h, double* out_f64, int64_t e_begin, int64_t e_end, void* stream) {
+                  double w_h, double* out_f64, double* partials, int64_t e_begin, int64_t e_end, void* stream) {
   if (!plan) return fail(DGM_ERR_INVALID, "null plan");
   const dgm_desc& d = plan->d;
-  if (!u || !mass_packed || !det_j || !out_f64 || !aligned16(u) || !aligned16(mass_packed))
+  if (!u || !mass_packed || !det_j || !out_f64 || !partials || !aligned16(u) || !aligned16(mass_packed))
     return fail(DGM_ERR_INVALID, "dgm_mass_norm: null or misaligned pointer");
   if (e_begin < 0 || e_end > d.num_elements || e_begin > e_end)
     return fail(DGM_ERR_INVALID, "element range outside the plan");
   if (e_end == e_begin) return DGM_OK;
+  DeviceGuard guard(plan->device);
   return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
     constexpr int N = decltype(n)::value;
     using T = decltype(t);
     using C = dgm::Cfg<N, T>;
     const int64_t tiles = (e_end - e_begin + C::TE - 1) / C::TE;
     const size_t msmem = (size_t)6 * C::TE * C::NPG * sizeof(T);
-    dgm::mass_norm_kernel<N, T><<<(unsigned)tiles, C::THREADS, msmem, static_cast<cudaStream_t>(stream)>>>(
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    dgm::mass_norm_kernel<N, T><<<(unsigned)tiles, C::THREADS, msmem, st>>>(
         static_cast<const T*>(u), static_cast<const T*>(mass_packed), static_cast<const T*>(det_j),
-        d.field_stride, e_begin, e_end, w_e, w_h, out_f64);
-    return cuda_check(cudaGetLastError(), "mass_norm_kernel launch");
+        d.field_stride, e_begin, e_end, w_e, w_h, partials);
+    if (int r = cuda_check(cudaGetLastError(), "mass_norm_kernel launch")) return r;
+    dgm::reduce_partials_kernel<<<1, 256, 0, st>>>(partials, tiles, out_f64);
+    return cuda_check(cudaGetLastError(), "reduce_partials_kernel launch");
   });
 }
 
-int dgm_pack(int32_t order, int32_t dtype, const double* natural, void* padded, int64_t num_elements,
-             int64_t field_stride, void* stream) {
+int64_t dgm_mass_norm_partials(const dgm_plan* plan, int64_t count) {
+  if (!plan || count < 0) return fail(DGM_ERR_INVALID, "dgm_mass_norm_partials: bad arguments");
+  int64_t te = 1;
+  dispatch(plan->d.order, plan->d.dtype, [&](auto n, auto t) -> int {
+    te = dgm::Cfg<decltype(n)::value, decltype(t)>::TE;
+    return DGM_OK;
+  });
+  return (count + te - 1) / te;
+}
+
+int dgm_face_states(const dgm_plan* plan, const void* u, const int64_t* elem_nat, const uint8_t* node_nat,
+                    void* u_minus, void* u_plus, void* stream) {
+  if (!plan || !u || !u_minus || !u_plus) return fail(DGM_ERR_INVALID, "dgm_face_states: null argument");
+  const dgm_desc& d = plan->d;
+  if (d.num_elements == 0) return DGM_OK;
+  DeviceGuard guard(plan->device);
+  return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    dgm::StageArgs<T> args = {};
+    args.u = static_cast<const T*>(u);
+    args.geo = static_cast<const T*>(d.geometry);
+    args.nbr = d.neighbors;
+    args.code = d.codes;
+    args.fmask = d.face_nodes;
+    args.ptab = d.code_table;
+    args.ncodes = d.num_codes;
+    args.kf = d.field_stride;
+    args.e_begin = 0;
+    args.e_end = d.num_elements;
+    dgm::face_states_kernel<N, T><<<grid_for(d.num_elements * 4 * C::NFP, 256), 256, 0,
+                                    static_cast<cudaStream_t>(stream)>>>(args, elem_nat, node_nat,
+                                                                         static_cast<T*>(u_minus),
+                                                                         static_cast<T*>(u_plus));
+    return cuda_check(cudaGetLastError(), "face_states_kernel launch");
+  });
+}
+
+int dgm_pack(int32_t order, int32_t dtype, const void* natural, int32_t natural_dtype, const int64_t* perm,
+             void* padded, int64_t num_elements, int64_t field_stride, void* stream) {
   if (!natural || !padded || num_elements < 0 || field_stride < num_elements)
     return fail(DGM_ERR_INVALID, "dgm_pack: bad arguments");
   if (num_elements == 0) return DGM_OK;
@@ -396,14 +465,18 @@ int dgm_pack(int32_t order, int32_t dtype, const double* natural, void* padded, 
     constexpr int N = decltype(n)::value;
     using T = decltype(t);
     using C = dgm::Cfg<N, T>;
-    dgm::pack_kernel<N, T><<<grid_for(6 * num_elements * C::NPG, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        natural, static_cast<T*>(padded), num_elements, field_stride);
-    return cuda_check(cudaGetLastError(), "pack_kernel launch");
+    return natural_dispatch(natural_dtype, [&](auto tn) -> int {
+      using TN = decltype(tn);
+      dgm::pack_kernel<N, T, TN><<<grid_for(6 * num_elements * C::NPG, 256), 256, 0,
+                                   static_cast<cudaStream_t>(stream)>>>(
+          static_cast<const TN*>(natural), perm, static_cast<T*>(padded), num_elements, field_stride);
+      return cuda_check(cudaGetLastError(), "pack_kernel launch");
+    });
   });
 }
 
-int dgm_unpack(int32_t order, int32_t dtype, const void* padded, double* natural, int64_t num_elements,
-               int64_t field_stride, void* stream) {
+int dgm_unpack(int32_t order, int32_t dtype, const void* padded, const int64_t* perm, void* natural,
+               int32_t natural_dtype, int64_t num_elements, int64_t field_stride, void* stream) {
   if (!natural || !padded || num_elements < 0 || field_stride < num_elements)
     return fail(DGM_ERR_INVALID, "dgm_unpack: bad arguments");
   if (num_elements == 0) return DGM_OK;
@@ -411,9 +484,13 @@ int dgm_unpack(int32_t order, int32_t dtype, const void* padded, double* natural
     constexpr int N = decltype(n)::value;
     using T = decltype(t);
     using C = dgm::Cfg<N, T>;
-    dgm::unpack_kernel<N, T><<<grid_for(6 * num_elements * C::NP, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const T*>(padded), natural, num_elements, field_stride);
-    return cuda_check(cudaGetLastError(), "unpack_kernel launch");
+    return natural_dispatch(natural_dtype, [&](auto tn) -> int {
+      using TN = decltype(tn);
+      dgm::unpack_kernel<N, T, TN><<<grid_for(6 * num_elements * C::NP, 256), 256, 0,
+                                     static_cast<cudaStream_t>(stream)>>>(
+          static_cast<const T*>(padded), perm, static_cast<TN*>(natural), num_elements, field_stride);
+      return cuda_check(cudaGetLastError(), "unpack_kernel launch");
+    });
   });
 }
 
@@ -425,6 +502,7 @@ int dgm_halo_pack(const dgm_plan* plan, const void* u, const int32_t* elements, 
     return fail(DGM_ERR_INVALID, "dgm_halo_pack: buffers must be 16-byte aligned");
   if (count == 0) return DGM_OK;
   const dgm_desc& d = plan->d;
+  DeviceGuard guard(plan->device);
   return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
     constexpr int N = decltype(n)::value;
     using T = decltype(t);
@@ -447,6 +525,7 @@ int dgm_halo_unpack(const dgm_plan* plan, const void* recvbuf, int64_t count, in
   if (!aligned16(u) || (recvbuf && !aligned16(recvbuf)))
     return fail(DGM_ERR_INVALID, "dgm_halo_unpack: buffers must be 16-byte aligned");
   if (count == 0) return DGM_OK;
+  DeviceGuard guard(plan->device);
   return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
     constexpr int N = decltype(n)::value;
     using T = decltype(t);

@@ -5,35 +5,89 @@
 
 namespace dgm {
 
-// natural float64 (6, K, NP) -> padded T (6, kf, NPG), zero padding
-// (reference fields.py:24-29 to_padded).
-template <int N, typename T>
-__global__ void pack_kernel(const double* __restrict__ nat, T* __restrict__ pad, int64_t k_total,
-                            int64_t kf) {
+// natural (6, K, NP) in TN (float64 as the reference, or float32) -> padded T (6, kf, NPG), zero
+// padding (reference fields.py:24-29 to_padded).  perm (NULL = identity) is the operator's internal
+// element order: padded slot s holds natural element perm[s] (the cast and the locality permutation
+// happen in this one pass).
+template <int N, typename T, typename TN>
+__global__ void pack_kernel(const TN* __restrict__ nat, const int64_t* __restrict__ perm, T* __restrict__ pad,
+                            int64_t k_total, int64_t kf) {
   using C = Cfg<N, T>;
   const int64_t total = 6 * k_total * C::NPG;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
        x += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = x / C::NPG;
     const int j = (int)(x - row * C::NPG);
-    const int64_t f = row / k_total, k = row - f * k_total;
-    const T v = (j < C::NP) ? (T)nat[row * C::NP + j] : T(0);
-    pad[(f * kf + k) * C::NPG + j] = v;
+    const int64_t f = row / k_total, s = row - f * k_total;
+    const int64_t k = perm ? __ldg(perm + s) : s;
+    const T v = (j < C::NP) ? (T)nat[(f * k_total + k) * C::NP + j] : T(0);
+    pad[(f * kf + s) * C::NPG + j] = v;
   }
 }
 
-// padded T -> natural float64 (fields.py:32-35 from_padded).
-template <int N, typename T>
-__global__ void unpack_kernel(const T* __restrict__ pad, double* __restrict__ nat, int64_t k_total,
-                              int64_t kf) {
+// padded T -> natural TN (fields.py:32-35 from_padded); natural element perm[s] <- padded slot s.
+template <int N, typename T, typename TN>
+__global__ void unpack_kernel(const T* __restrict__ pad, const int64_t* __restrict__ perm, TN* __restrict__ nat,
+                              int64_t k_total, int64_t kf) {
   using C = Cfg<N, T>;
   const int64_t total = 6 * k_total * C::NP;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
        x += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = x / C::NP;
     const int j = (int)(x - row * C::NP);
-    const int64_t f = row / k_total, k = row - f * k_total;
-    nat[x] = (double)pad[(f * kf + k) * C::NPG + j];
+    const int64_t f = row / k_total, s = row - f * k_total;
+    const int64_t k = perm ? __ldg(perm + s) : s;
+    nat[(f * k_total + k) * C::NP + j] = (TN)pad[(f * kf + s) * C::NPG + j];
+  }
+}
+
+// face_states (oracle.py:50-58): u_minus / u_plus per (field, element, face, face node) in the natural
+// numbering, with the PEC mirror (maxwell.py:117-132) on walls.  Internal slot s is natural element
+// elem_nat[s] (NULL = identity); internal face slot q of face f is natural face node
+// node_nat[f * NFP + q] (NULL = identity; ordering.face_slot_order).
+template <int N, typename T>
+__global__ void face_states_kernel(const StageArgs<T> a, const int64_t* __restrict__ elem_nat,
+                                   const uint8_t* __restrict__ node_nat, T* __restrict__ u_minus,
+                                   T* __restrict__ u_plus) {
+  using C = Cfg<N, T>;
+  constexpr int NFP = C::NFP, NPG = C::NPG;
+  const int64_t k_total = a.e_end;  // whole owned range
+  const int64_t total = k_total * 4 * NFP;
+  const int64_t fstride = a.kf * NPG;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = x / (4 * NFP);
+    const int r = (int)(x - s * 4 * NFP), face = r / NFP, q = r - face * NFP;
+    const T* gk = a.geo + s * GEO_WORDS;
+    const T nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
+    const int im = a.fmask[face * NFP + q];
+    T um[6], up[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) um[f] = a.u[f * fstride + s * NPG + im];
+    const int code = a.code[s * 4 + face];
+    if (code < 0) {
+      const T nde = nx * um[0] + ny * um[1] + nz * um[2];
+      const T ndh = nx * um[3] + ny * um[4] + nz * um[5];
+      up[0] = -um[0] + T(2) * nde * nx;
+      up[1] = -um[1] + T(2) * nde * ny;
+      up[2] = -um[2] + T(2) * nde * nz;
+      up[3] = um[3] - T(2) * ndh * nx;
+      up[4] = um[4] - T(2) * ndh * ny;
+      up[5] = um[5] - T(2) * ndh * nz;
+    } else {
+      const int64_t nb = a.nbr[s * 4 + face];
+      const int jn = a.ptab[code * NFP + q];
+#pragma unroll
+      for (int f = 0; f < 6; ++f) up[f] = a.u[f * fstride + nb * NPG + jn];
+    }
+    const int64_t k = elem_nat ? elem_nat[s] : s;
+    const int node = node_nat ? node_nat[face * NFP + q] : q;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      const int64_t o = ((f * k_total + k) * 4 + face) * NFP + node;
+      u_minus[o] = um[f];
+      u_plus[o] = up[f];
+    }
   }
 }
 
@@ -75,12 +129,14 @@ __global__ void halo_unpack_kernel(const T* __restrict__ recv, int64_t count, in
   }
 }
 
-// *out += sum_k J_k sum_f w_f u_fk^T M u_fk   (maxwell.py:211-232)
+// partial[blockIdx] = sum over the CTA's elements of J_k sum_f w_f u_fk^T M u_fk   (maxwell.py:211-232);
+// reduce_partials_kernel adds them into *out in a fixed order, so the value is bitwise reproducible
+// (the reference's CLI reruns are byte-identical, pkg/tests/test_cli.py:106-112)
 template <int N, typename T>
 __global__ void __launch_bounds__(Cfg<N, T>::THREADS)
 mass_norm_kernel(const T* __restrict__ u, const T* __restrict__ mass, const T* __restrict__ det_j,
                  int64_t kf, int64_t e_begin, int64_t e_end, double w_e, double w_h,
-                 double* __restrict__ out) {
+                 double* __restrict__ partial) {
   using C = Cfg<N, T>;
   using V = typename V16<T>::type;
   constexpr int TE = C::TE, NPG = C::NPG, NP = C::NP, VEC = C::VEC, G = C::G, E = C::E;
@@ -137,7 +193,24 @@ mass_norm_kernel(const T* __restrict__ u, const T* __restrict__ mass, const T* _
   if (tid < 32) {
     double v = (tid < (int)(blockDim.x >> 5)) ? s_red[tid] : 0.0;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (tid == 0) atomicAdd(out, v);
+    if (tid == 0) partial[blockIdx.x] = v;
+  }
+}
+
+// *out += sum_i partial[i], one CTA: thread t sums i = t, t + 256, ... in order, then a fixed
+// shuffle / shared-memory tree -- the same association for every launch of the same count.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ partial, int64_t n,
+                                                              double* __restrict__ out) {
+  __shared__ double s_red[8];
+  double v = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) v += partial[i];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += s_red[w];
+    *out += t;
   }
 }
 

@@ -224,6 +224,7 @@ class DistributedMaxwellOperator:
         self._recv = {p: torch.empty((cnt, rows), dtype=dtype, device=self.device)
                       for p, (_, cnt) in domain.recv.items()}
         self._alt = self.op.empty_state()
+        self._alt2 = self.op.empty_state()
         self._res = self.op.empty_state()
 
     @staticmethod
@@ -323,13 +324,12 @@ class DistributedMaxwellOperator:
 
         if dt <= 0.0:
             raise ValueError("dt must be positive")
-        cur, nxt = u, self._alt
-        for _ in range(int(nsteps)):
-            for a, b in zip(RK_A, RK_B):
-                self._stage(cur, nxt, a, b, dt)
-                cur, nxt = nxt, cur
-        if cur is not u:
-            u.copy_(cur)
+        for _ in range(int(nsteps)):  # u -> alt -> alt2 -> alt -> alt2 -> u, as B200MaxwellOperator
+            src = u
+            for i, (a, b) in enumerate(zip(RK_A, RK_B)):
+                dst = u if i == len(RK_A) - 1 else (self._alt if i % 2 == 0 else self._alt2)
+                self._stage(src, dst, a, b, dt)
+                src = dst
         return u
 
     def rhs_padded(self, u, out=None):

@@ -77,7 +77,10 @@ def _face_slot_order(elem: ReferenceElement) -> np.ndarray:
     from .ordering import face_slot_order
 
     if elem.order not in _SLOT_ORDERS:  # modelled on the fp32 tensor kernel's strides (TcCfg<N>)
-        npg, nfpk = (elem.num_nodes + 3) // 4 * 4, (elem.num_face_nodes + 7) // 8 * 8
+        # the shared-memory row stride the kernel really uses (TcCfg::NPG = the f32 np_stride, an odd
+        # number of 16-byte chunks), not ceil4(Np): they differ at N = 5, 7, 8
+        npg = _capi.layout(elem.order, _capi.DGM_F32).np_stride
+        nfpk = (elem.num_face_nodes + 7) // 8 * 8
         _SLOT_ORDERS[elem.order] = face_slot_order(elem.face_nodes, elem.order, npg, nfpk)
     return _SLOT_ORDERS[elem.order]
 
@@ -95,8 +98,11 @@ def geometry_words(geometry: GeometricFactors) -> np.ndarray:
 
 @dataclass
 class _Buffers:
+    """LSRK4 scratch: two state registers (a step runs u -> alt -> alt2 -> alt -> alt2 -> u) + residual."""
+
     alt: torch.Tensor
     res: torch.Tensor
+    alt2: torch.Tensor | None = None
 
 
 @dataclass
@@ -152,6 +158,7 @@ class B200MaxwellOperator:
             face_slots = bool(lay.tc_supported) and path != "simt"
         lift = elem.lift
         self._slot_inv = None
+        self._slot_nat = None  # uint8 [4][Nfp]: internal face slot -> natural face node (dgm_face_states)
         if face_slots:
             from .ordering import permute_face_slots
 
@@ -163,6 +170,7 @@ class B200MaxwellOperator:
             inv = np.empty_like(cols)
             inv[cols] = np.arange(len(cols))
             self._slot_inv = torch.as_tensor(inv, device=self.device)
+            self._slot_nat = torch.as_tensor(np.ascontiguousarray(perm, dtype=np.uint8).reshape(-1), device=self.device)
 
         def dev(a, dt=dtype):
             return torch.as_tensor(np.ascontiguousarray(a)).to(device=self.device, dtype=dt)
@@ -209,6 +217,8 @@ class B200MaxwellOperator:
         self._bufs: _Buffers | None = None
         self._graphs: dict = {}
         self._norm_out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        n_part = int(lib.dgm_mass_norm_partials(handle, self.num_elements))
+        self._partials = torch.zeros(max(n_part, 1), dtype=torch.float64, device=self.device)
         self.collect_stats = False   # record CUDA-event times of every stage launch
         self._events: list = []
         self._stats: dict = {}
@@ -283,17 +293,27 @@ class B200MaxwellOperator:
         launch()
         stop.record(stream)
         self._events.append((name, start, stop))
+        if len(self._events) >= 256:
+            self._drain_events(block=False)
+
+    def _drain_events(self, block: bool) -> None:
+        """Fold recorded event pairs into the per-kernel totals (completed ones only unless ``block``)."""
+        if block and self._events:
+            torch.cuda.synchronize(self.device)
+        done = 0
+        for name, start, stop in self._events:
+            if not block and not stop.query():
+                break
+            st = self._stats.setdefault(name, KernelStats())
+            st.launches += 1
+            st.ms += start.elapsed_time(stop)
+            done += 1
+        del self._events[:done]
 
     @property
     def stage_stats(self) -> dict:
         """Per-kernel device time {name: KernelStats} (pipeline.py:62-68's stage_stats, measured)."""
-        if self._events:
-            torch.cuda.synchronize(self.device)
-            for name, start, stop in self._events:
-                st = self._stats.setdefault(name, KernelStats())
-                st.launches += 1
-                st.ms += start.elapsed_time(stop)
-            self._events.clear()
+        self._drain_events(block=True)
         return self._stats
 
     def reset_stats(self) -> None:
@@ -321,32 +341,59 @@ class B200MaxwellOperator:
         if u.dtype != self.dtype or u.device != self.device or not u.is_contiguous():
             raise ValueError(f"{name} must be a contiguous {self.dtype} tensor on {self.device}")
 
-    def to_padded(self, natural, out: torch.Tensor | None = None) -> torch.Tensor:
-        """Natural (6, K, Np) numpy/torch -> padded device tensor (padding zero)."""
+    def _natural_tensor(self, natural) -> torch.Tensor:
+        """Natural state as a device tensor of shape (6, K, Np), float32 or float64 (reshape as oracle.py:65)."""
         k, n_p = self.num_elements, self.elem.num_nodes
         src = torch.as_tensor(natural)
-        if tuple(src.shape) != (N_FIELDS, k, n_p):
-            raise ValueError(f"natural state must have shape (6, {k}, {n_p}), got {tuple(src.shape)}")
-        src = src.to(device=self.device, dtype=torch.float64)
-        src = (src if self._order is None else src.index_select(1, self._order)).contiguous()
+        if src.numel() != N_FIELDS * k * n_p:
+            raise ValueError(f"natural state must have 6*K*Np = {N_FIELDS * k * n_p} values "
+                             f"(shape (6, {k}, {n_p})), got shape {tuple(src.shape)}")
+        if src.dtype not in (torch.float32, torch.float64):
+            src = src.to(torch.float64)
+        src = src.reshape(N_FIELDS, k, n_p)
+        if src.device != self.device:
+            src = src.to(self.device, non_blocking=src.is_pinned())
+        return src.contiguous()
+
+    def to_padded(self, natural, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Natural (6, K, Np) numpy/torch (float32 or float64) -> padded device tensor (padding zero).
+
+        The dtype cast and the internal element order are applied by the pack kernel itself.
+        """
+        src = self._natural_tensor(natural)
         if out is None:
             out = self.empty_state()
         else:
             self._check_padded(out, "out")
-        _capi.check(self._lib.dgm_pack(self.order, self._dt_code, src.data_ptr(), out.data_ptr(), k,
-                                       self.field_stride, self._stream()), "dgm_pack")
+        nat_dt = _capi.DGM_F32 if src.dtype == torch.float32 else _capi.DGM_F64
+        perm = self._order.data_ptr() if self._order is not None else None
+        with torch.cuda.device(self.device):
+            _capi.check(self._lib.dgm_pack(self.order, self._dt_code, src.data_ptr(), nat_dt, perm, out.data_ptr(),
+                                           self.num_elements, self.field_stride, self._stream()), "dgm_pack")
         return out
 
-    def from_padded(self, padded: torch.Tensor, dtype: torch.dtype = torch.float64) -> torch.Tensor:
-        """Padded device tensor -> natural (6, K, Np) device tensor (float64 as the reference, or ``dtype``)."""
+    def from_padded(self, padded: torch.Tensor, dtype: torch.dtype = torch.float64,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
+        """Padded device tensor -> natural (6, K, Np) device tensor (float64 as the reference, or float32).
+
+        Cast and inverse element permutation happen in the unpack kernel; ``out`` (a contiguous natural
+        tensor of that dtype on the device) is filled in place when given.
+        """
         self._check_padded(padded, "padded")
-        out = torch.empty((N_FIELDS, self.num_elements, self.elem.num_nodes), dtype=torch.float64,
-                          device=self.device)
-        _capi.check(self._lib.dgm_unpack(self.order, self._dt_code, padded.data_ptr(), out.data_ptr(),
-                                         self.num_elements, self.field_stride, self._stream()), "dgm_unpack")
-        if self._inv is not None:
-            out = out.index_select(1, self._inv)  # back to the natural (reference) numbering
-        return out if dtype == torch.float64 else out.to(dtype)
+        if dtype not in (torch.float32, torch.float64):
+            raise ValueError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
+        shape = (N_FIELDS, self.num_elements, self.elem.num_nodes)
+        if out is None:
+            out = torch.empty(shape, dtype=dtype, device=self.device)
+        elif tuple(out.shape) != shape or out.dtype != dtype or out.device != self.device or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous {dtype} tensor of shape {shape} on {self.device}")
+        nat_dt = _capi.DGM_F32 if dtype == torch.float32 else _capi.DGM_F64
+        perm = self._order.data_ptr() if self._order is not None else None
+        with torch.cuda.device(self.device):
+            _capi.check(self._lib.dgm_unpack(self.order, self._dt_code, padded.data_ptr(), perm, out.data_ptr(),
+                                             nat_dt, self.num_elements, self.field_stride, self._stream()),
+                        "dgm_unpack")
+        return out
 
     def check_padding(self, padded: torch.Tensor) -> bool:
         """True when every padding slot is exactly zero (fields.py:55-58)."""
@@ -392,13 +439,38 @@ class B200MaxwellOperator:
         return out if self._inv is None else out.index_select(1, self._inv)  # natural numbering
 
     def rhs(self, state):
-        """Reference-compatible RHS: natural (6, K, Np) in, new array of the same kind out."""
+        """Reference-compatible RHS (oracle.py:60-94): natural state in (any shape holding 6*K*Np values,
+        reshaped as the reference does), new (6, K, Np) array of the same kind out (numpy stays numpy,
+        torch stays on its device), float32 input -> float32 output, anything else -> float64."""
         is_numpy = not isinstance(state, torch.Tensor)
-        u = self.to_padded(state)
-        out = self.from_padded(self.rhs_padded(u))
+        src = np.asarray(state) if is_numpy else state
+        out_dtype = torch.float32 if (src.dtype == np.float32 if is_numpy else src.dtype == torch.float32) \
+            else torch.float64
+        u = self.to_padded(src)
+        out = self.from_padded(self.rhs_padded(u), out_dtype)
         if is_numpy:
             return out.cpu().numpy()
         return out.to(device=state.device)
+
+    def face_states(self, state):
+        """(u_minus, u_plus, normals) per face node, boundary side mirrored (oracle.py:50-58).
+
+        u_minus / u_plus are (6, K, 4, Nfp) gathered on the device by dgm_face_states in the natural
+        numbering; normals are (3, K, 4, 1).  numpy in -> numpy out (float64), torch in -> torch out.
+        """
+        is_numpy = not isinstance(state, torch.Tensor)
+        u = self.to_padded(np.asarray(state) if is_numpy else state)
+        shape = (N_FIELDS, self.num_elements, NUM_FACES, self.elem.num_face_nodes)
+        um = torch.empty(shape, dtype=self.dtype, device=self.device)
+        up = torch.empty_like(um)
+        perm = self._order.data_ptr() if self._order is not None else None
+        nodes = self._slot_nat.data_ptr() if self._slot_nat is not None else None
+        _capi.check(self._lib.dgm_face_states(self._plan, u.data_ptr(), perm, nodes, um.data_ptr(), up.data_ptr(),
+                                              self._stream()), "dgm_face_states")
+        nrm = np.moveaxis(self.geometry.normals, -1, 0)[:, :, :, None]
+        if is_numpy:
+            return um.double().cpu().numpy(), up.double().cpu().numpy(), nrm
+        return um.to(state.device), up.to(state.device), torch.as_tensor(nrm, device=state.device)
 
     rhs_natural = rhs
 
@@ -416,26 +488,35 @@ class B200MaxwellOperator:
         return self._bufs
 
     def workspace(self) -> _Buffers:
-        """Scratch registers (ping-pong state + LSRK residual) for ``advance(..., workspace=)``.
+        """Scratch registers (two state buffers + LSRK residual) for ``advance(..., workspace=)``.
 
         The operator keeps one of its own; pass a separate workspace per CUDA stream to advance
         independent states concurrently.
         """
-        return _Buffers(alt=self.empty_state(), res=self.empty_state())
+        return _Buffers(alt=self.empty_state(), res=self.empty_state(), alt2=self.empty_state())
 
     def _launch_steps(self, u: torch.Tensor, dt: float, nsteps: int, bufs: _Buffers | None = None) -> torch.Tensor:
-        """nsteps LSRK4 steps ping-ponging u <-> alt; returns the tensor holding the result."""
+        """nsteps LSRK4 steps, each ending back in u: u -> alt -> alt2 -> alt -> alt2 -> u.
+
+        A stage cannot update in place (neighbour traces read u_in while other CTAs write u_out); with
+        two scratch registers the odd stage count of a step still lands in u, so no copy is needed.
+        """
         bufs = self._buffers() if bufs is None else bufs
-        cur, nxt = u, bufs.alt
+        if bufs.alt2 is None:
+            bufs.alt2 = self.empty_state()
         for _ in range(nsteps):
-            for a, b in zip(RK_A, RK_B):
-                self.lsrk_stage(cur, nxt, bufs.res, a, b, dt)
-                cur, nxt = nxt, cur
-        return cur
+            src = u
+            for i, (a, b) in enumerate(zip(RK_A, RK_B)):
+                dst = u if i == len(RK_A) - 1 else (bufs.alt if i % 2 == 0 else bufs.alt2)
+                self.lsrk_stage(src, dst, bufs.res, a, b, dt)
+                src = dst
+        return u
+
+    GRAPH_STEPS = 8  # LSRK4 steps per captured CUDA graph
 
     def advance(self, u: torch.Tensor, dt: float, nsteps: int = 1, use_graph: bool | None = None,
                 workspace: _Buffers | None = None) -> torch.Tensor:
-        """Advance the padded state in place by nsteps LSRK4 steps of size dt."""
+        """Advance the padded state in place by nsteps LSRK4 steps of size dt (no copies)."""
         self._check_padded(u)
         if dt <= 0.0:
             raise ValueError("dt must be positive")
@@ -448,32 +529,27 @@ class B200MaxwellOperator:
             use_graph = nsteps >= 4
         bufs = self._buffers() if workspace is None else workspace
         if not use_graph:
-            cur = self._launch_steps(u, dt, nsteps, bufs)
-            if cur is not u:
-                u.copy_(cur)
-            return u
-        pairs, odd = divmod(nsteps, 2)
-        if pairs:
-            graph = self._graph_for(u, dt, bufs)
-            for _ in range(pairs):
-                graph.replay()
-        if odd:
-            cur = self._launch_steps(u, dt, 1, bufs)
-            u.copy_(cur)
+            return self._launch_steps(u, dt, nsteps, bufs)
+        chunks, rest = divmod(nsteps, self.GRAPH_STEPS)
+        for _ in range(chunks):
+            self._graph_for(u, dt, bufs, self.GRAPH_STEPS).replay()
+        if rest:
+            self._graph_for(u, dt, bufs, rest).replay()
         return u
 
-    def _graph_for(self, u: torch.Tensor, dt: float, bufs: _Buffers):
-        """CUDA graph of two LSRK4 steps (10 stage launches, u -> alt -> ... -> u)."""
-        key = (u.data_ptr(), bufs.alt.data_ptr(), float(dt))
+    def _graph_for(self, u: torch.Tensor, dt: float, bufs: _Buffers, nsteps: int):
+        """CUDA graph of ``nsteps`` LSRK4 steps (5 * nsteps stage launches, u -> ... -> u)."""
+        if bufs.alt2 is None:
+            bufs.alt2 = self.empty_state()
+        key = (u.data_ptr(), bufs.alt.data_ptr(), bufs.alt2.data_ptr(), bufs.res.data_ptr(), float(dt), nsteps)
         graph = self._graphs.get(key)
         if graph is None:
             # load the stage kernel outside capture (scratch buffers only)
-            self.lsrk_stage(u, bufs.alt, bufs.res, 0.0, 0.0, 0.0, 0, min(self.num_elements, 1))
+            self.lsrk_stage(bufs.alt, bufs.alt2, bufs.res, 0.0, 0.0, 0.0, 0, min(self.num_elements, 1))
             torch.cuda.current_stream(self.device).synchronize()
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
-                cur = self._launch_steps(u, dt, 2, bufs)
-                assert cur is u
+                self._launch_steps(u, dt, nsteps, bufs)
             self._graphs[key] = graph
         return graph
 
@@ -486,7 +562,9 @@ class B200MaxwellOperator:
                   out: torch.Tensor | None = None) -> torch.Tensor:
         """Device scalar sum_k J_k sum_f w_f u^T M u (float64 tensor, no sync).
 
-        With ``out`` (a zeroed float64 device slot) the value is accumulated there.
+        With ``out`` (a zeroed float64 device slot) the value is accumulated there.  The reduction
+        order is fixed (per-CTA partials, then one fixed-order pass), so reruns are bitwise identical.
+        Calls on one operator share the partials scratch: issue them on one stream.
         """
         self._check_padded(u)
         if out is None:
@@ -494,8 +572,8 @@ class B200MaxwellOperator:
         elif out.dtype != torch.float64 or out.device != self.device or out.numel() < 1:
             raise ValueError("out must be a float64 device tensor on the operator's device")
         _capi.check(self._lib.dgm_mass_norm(self._plan, u.data_ptr(), self._mass.data_ptr(), self._det.data_ptr(),
-                                            float(w_e), float(w_h), out.data_ptr(), 0, self.num_elements,
-                                            self._stream()), "dgm_mass_norm")
+                                            float(w_e), float(w_h), out.data_ptr(), self._partials.data_ptr(),
+                                            0, self.num_elements, self._stream()), "dgm_mass_norm")
         return out
 
     def field_energy(self, u: torch.Tensor) -> float:

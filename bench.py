@@ -10,8 +10,13 @@ explicit flush is needed between steps.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
 --gpus N > 1 runs under torchrun, one rank per GPU (NCCL); see DESIGN.md.
---impl reference times the reference algorithm (the numpy oracle port of
-simtdg's ReferenceMaxwellOperator.rhs + rk4_step) on the host cores.
+--impl reference times the reference itself (simtdg's build_reference_operator
+.rhs inside its rk4_step, installed into baseline/_ref by
+scripts/install_reference.sh; the oracle port if absent) on the host cores.
+
+The N=1 line also carries the other BASELINE configs (C1 through the CUDA-graph
+path, a C2 order subset, C3 fp64, C5 N=6) under "configs", each with its own
+clocks and a max(B_alg/BW, F_alg/P) roofline; --extras selects them.
 """
 
 from __future__ import annotations
@@ -32,7 +37,6 @@ METRIC = "Maxwell DG net GFLOP/s & DOF-updates/s per RK4 step (N=4, tets); HBM G
 UNIT = "GFLOP/s"
 ORDER = 4
 CELLS = (55, 55, 55)
-CPU_SAMPLE_CELLS = (6, 6, 7)
 
 
 def _flatten(d, prefix=""):
@@ -103,6 +107,7 @@ class ClockSampler:
         self.proc = None
         self.samples = []  # (arrival time, line)
         self.t0 = self.t1 = None
+        self.windows = {}  # name -> [t0, t1] of an extra config's timed region
 
     def __enter__(self):
         import threading
@@ -127,11 +132,18 @@ class ClockSampler:
             time.sleep(0.02)
         return self
 
-    def mark_start(self):
-        self.t0 = time.time()
+    def mark_start(self, name: str | None = None):
+        if name is None:
+            self.t0 = time.time()
+        else:
+            self.windows[name] = [time.time(), None]
 
-    def mark_stop(self):
-        self.t1 = time.time() + 0.1  # the line reporting the last timed interval arrives a period later
+    def mark_stop(self, name: str | None = None):
+        t = time.time() + 0.1  # the line reporting the last timed interval arrives a period later
+        if name is None:
+            self.t1 = t
+        else:
+            self.windows[name][1] = t
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -142,8 +154,9 @@ class ClockSampler:
                 self.proc.kill()
             self.thread.join(timeout=5)
 
-    def summary(self) -> dict:
-        lines = [l for t, l in self.samples if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
+    def summary(self, name: str | None = None) -> dict:
+        t0, t1 = (self.t0, self.t1) if name is None else self.windows.get(name, (None, None))
+        lines = [l for t, l in self.samples if t0 is not None and t0 <= t <= (t1 or t)]
         window = "timed"
         if not lines:
             lines, window = [l for _, l in self.samples], "run"
@@ -172,54 +185,279 @@ def _dist_env():
     return world, rank, local
 
 
-def cpu_reference_rate(order: int, cells, steps: int, warmup: int = 0):
-    """Time the oracle port (reference algorithm, single thread) on a bounded sample."""
+# ----------------------------------------------------------------------------------------------
+# CPU reference: the genuine simtdg (baseline/_ref, installed by scripts/install_reference.sh) when
+# present, else the oracle port.  One single-threaded process per host core, each integrating its
+# own x-slab of the C2 box (20^3 cells, 48,000 tets in total) with the reference's own
+# build_reference_operator + rk4_step (numpy einsum is single-threaded, so processes are how the
+# reference uses all host cores); rate = all workers' work / the slowest worker's time.
+# ----------------------------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+CPU_SAMPLE_BOX = (20, 20, 20)
+CPU_MAX_ELEMENTS_PER_WORKER = 7200  # ~2.5 s per N=4 step per worker: the whole run stays within minutes
+
+
+def _host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def _ref_available() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "simtdg"))
+
+
+def _cpu_worker(kind, order, cx, x0, steps, warmup, barrier, queue):
+    """One reference process: slab [x0, x0 + cx) x 20 x 20 cells of the unit C2 box."""
     import numpy as np
 
-    from oracle import build_oracle_operator, rk4_step
-    from paper_0901_1024_b200 import (CavityMode, build_reference_element, compute_geometry, generate_box_mesh,
-                                      map_nodes, stable_dt)
-    from paper_0901_1024_b200.perfmodel import flops_per_element_stage
-
-    mesh = generate_box_mesh((1.0, 1.0, 1.0), cells)
+    if kind == "reference":
+        sys.path.insert(0, REF_DIR)
+        from simtdg.kernels.assemble import rk4_step
+        from simtdg.kernels.oracle import build_reference_operator as build
+        from simtdg.maxwell import CavityMode, stable_dt
+        from simtdg.mesh import generate_box_mesh
+        from simtdg.refelem import build_reference_element
+    else:
+        from oracle import build_oracle_operator as build
+        from oracle import rk4_step
+        from paper_0901_1024_b200 import CavityMode, build_reference_element, generate_box_mesh, stable_dt
+    nx = CPU_SAMPLE_BOX[0]
+    mesh = generate_box_mesh((cx / nx, 1.0, 1.0), (cx, CPU_SAMPLE_BOX[1], CPU_SAMPLE_BOX[2]))
+    mesh.vertices[:, 0] += x0 / nx
     elem = build_reference_element(order)
-    ora = build_oracle_operator(mesh, elem)
-    u = CavityMode(1, 1, 1, (1.0, 1.0, 1.0)).evaluate(map_nodes(mesh, elem), 0.0)
-    dt = stable_dt(mesh, compute_geometry(mesh), order)
+    op = build(mesh, elem)
+    u = CavityMode(1, 1, 1, extent=(1.0, 1.0, 1.0)).evaluate(op.nodes, 0.0)
+    dt = stable_dt(mesh, op.geometry, order)
     for _ in range(warmup):
-        u = rk4_step(u, 0.0, dt, lambda t, y: ora.rhs(y))
+        u = rk4_step(u, 0.0, dt, lambda t, y: op.rhs(y))
+    barrier.wait()
     t0 = time.perf_counter()
     for _ in range(steps):
-        u = rk4_step(u, 0.0, dt, lambda t, y: ora.rhs(y))
+        u = rk4_step(u, 0.0, dt, lambda t, y: op.rhs(y))
     sec = time.perf_counter() - t0
-    k = mesh.num_elements
+    queue.put((int(mesh.elements.shape[0]), sec, bool(np.isfinite(u).all())))
+
+
+def cpu_reference_rate(order: int, steps: int, warmup: int = 0, workers: int | None = None) -> dict:
+    """Time the reference path on the host cores (see the block comment above)."""
+    import multiprocessing as mp
+
+    from paper_0901_1024_b200.perfmodel import flops_per_element_stage
+    from paper_0901_1024_b200.refelem import simplex_node_count
+
+    kind = "reference" if _ref_available() else "port"
+    cores = _host_cores()
+    p = max(1, min(workers or cores, CPU_SAMPLE_BOX[0]))
+    nx, ny, nz = CPU_SAMPLE_BOX
+    per_x = 6 * ny * nz
+    # slabs of >= 1 x-cell, at most CPU_MAX_ELEMENTS_PER_WORKER tets each (smaller sample on few cores)
+    cx_max = max(1, CPU_MAX_ELEMENTS_PER_WORKER // per_x)
+    total_x = min(nx, p * cx_max)
+    base, extra = divmod(total_x, p)
+    slabs, x0 = [], 0
+    for i in range(p):
+        cx = base + (1 if i < extra else 0)
+        if cx:
+            slabs.append((cx, x0))
+            x0 += cx
+    env_keep = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in env_keep:
+        os.environ[k] = "1"  # one core per worker (inherited by the spawned processes)
+    ctx = mp.get_context("spawn")
+    barrier, queue = ctx.Barrier(len(slabs)), ctx.Queue()
+    procs = [ctx.Process(target=_cpu_worker, args=(kind, order, cx, x0, steps, warmup, barrier, queue))
+             for cx, x0 in slabs]
+    try:
+        for pr in procs:
+            pr.start()
+        res = [queue.get(timeout=1800) for _ in procs]
+        for pr in procs:
+            pr.join()
+    finally:
+        for k, v in env_keep.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    if not all(r[2] for r in res):
+        raise RuntimeError("non-finite state in the CPU reference run")
+    k = sum(r[0] for r in res)
+    sec = max(r[1] for r in res)
+    n_p = simplex_node_count(order)[0]
     flops = flops_per_element_stage(order) * k * 5 * steps
-    dof = 6 * elem.num_nodes * k * steps
-    assert np.isfinite(u).all()
-    return {"gflops": flops / sec / 1e9, "dof_updates_per_s": dof / sec, "seconds": sec, "elements": k,
-            "steps": steps}
+    path = ("genuine simtdg 0.1.0 (baseline/_ref) build_reference_operator().rhs inside simtdg rk4_step"
+            if kind == "reference" else "oracle port (oracle/dg_oracle.py) of simtdg rhs + rk4_step")
+    sample = (f"{len(slabs)} single-threaded processes x one x-slab each of the C2 box {CPU_SAMPLE_BOX} "
+              f"({k} tets in total, N={order}), {steps} LSRK4 steps after {warmup} warm-up; {path}; "
+              f"rate per DOF is nearly K-independent, so it stands for the named config")
+    return {"gflops": flops / sec / 1e9, "dof_updates_per_s": 6 * n_p * k * steps / sec, "seconds": sec,
+            "elements": k, "steps": steps, "kind": kind, "cores": len(slabs), "host_cores": cores,
+            "sample": sample}
 
 
 def run_reference(args) -> None:
     world, rank, _ = _dist_env()
     if rank != 0:
         return
-    r = cpu_reference_rate(ORDER, CPU_SAMPLE_CELLS, args.steps, args.warmup)
-    sample = (f"box {CPU_SAMPLE_CELLS} -> {r['elements']} tets, N={ORDER}, {args.steps} LSRK4 steps after "
-              f"{args.warmup} warm-up (the full {CELLS} workload needs ~44 GB and ~7 min per step on this path); "
-              "rate is per-DOF and nearly K-independent")
+    r = cpu_reference_rate(args.order, args.steps, args.warmup)
     line = {
         "metric": METRIC, "value": r["gflops"], "unit": UNIT, "impl": "reference", "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "dof_updates_per_s": r["dof_updates_per_s"],
-        "config": {"workload": f"C3 Maxwell PEC cavity N={ORDER}, box {CELLS}", "order": ORDER,
-                   "sample_elements": r["elements"], "path": "oracle port of simtdg ReferenceMaxwellOperator.rhs "
-                   "+ rk4_step (numpy einsum, single-threaded as the reference)"},
-        "cpu_baseline": {"value": r["gflops"], "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "config": {"workload": f"C3 Maxwell PEC cavity N={args.order}, box {tuple(args.cells)} (per-DOF rate "
+                               f"on a bounded sample, see cpu_baseline.sample)", "order": args.order,
+                   "sample_elements": r["elements"], "host_cores": r["host_cores"]},
+        "cpu_baseline": {"value": r["gflops"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                         "host_cores": r["host_cores"], "sample": r["sample"]},
         "e2e": {"value": r["gflops"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------------
+# Roofline: T_roof = max(B_alg / BW, F_alg / P) per element-stage (SURVEY 8(d)); P is the peak of
+# the pipe the kernel computes on: the measured kind::tf32 MMA rate / 3 for the 3xTF32 tensor path,
+# FP32 or FP64 SIMT (148 SMs x 128 / 64 lanes x 2 flop x clock) otherwise.
+# ----------------------------------------------------------------------------------------------
+def measure_tf32_tflops(dev, sm_mhz: float) -> dict | None:
+    """kind::tf32 MMA throughput of one SM (probe library, M=128 N=48 K=8 TS bursts) x SMs x clock."""
+    import ctypes
+
+    import torch
+
+    path = os.path.join(ROOT, "paper_0901_1024_b200", "libdgm_probe.so")
+    try:
+        lib = ctypes.CDLL(path)
+    except OSError:
+        return None
+    lib.dgm_probe_mma_rate.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p]
+    out = torch.zeros(2, dtype=torch.int64, device=dev)
+    best = None
+    with torch.cuda.device(dev):
+        for _ in range(3):
+            if lib.dgm_probe_mma_rate(48, 960, 1, 0, out.data_ptr()) != 0:
+                return None
+            torch.cuda.synchronize(dev)
+            clk = out[1].item() / 960.0
+            best = clk if best is None else min(best, clk)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    flop_clk = 128 * 48 * 8 * 2 / best
+    return {"tflops": flop_clk * sms * sm_mhz * 1e6 / 1e12, "clk_per_mma": best, "sms": sms,
+            "source": "probe: tcgen05.mma kind::tf32 M=128 N=48 K=8 (A in TMEM) bursts, measured in this run"}
+
+
+def roofline(order, word, path, k, launch_s, peaks, pipes, kernel, traffic):
+    from paper_0901_1024_b200.perfmodel import bytes_per_element_stage, flops_per_element_stage
+
+    b = bytes_per_element_stage(order, word) * k
+    f = flops_per_element_stage(order) * k
+    bw = peaks["hbm_gbs"] * 1e9
+    if path == "tensor" and pipes.get("tf32"):
+        p, pipe = pipes["tf32"]["tflops"] * 1e12 / 3.0, "tensor"
+        psrc = "3xTF32: measured kind::tf32 rate / 3 (" + pipes["tf32"]["source"] + ")"
+    elif word == 8:
+        p, pipe, psrc = pipes["fp64_tflops"] * 1e12, "fp64", "FP64 SIMT: SMs x 64 x 2 x max SM clock"
+    else:
+        p, pipe, psrc = pipes["fp32_tflops"] * 1e12, "fp32", "FP32 SIMT: SMs x 128 x 2 x max SM clock"
+    t_mem, t_cmp = b / bw, f / p
+    hbm = t_mem >= t_cmp
+    return {"bound": "hbm" if hbm else pipe,
+            "achieved": (b if hbm else f) / launch_s / (1e9 if hbm else 1e12),
+            "peak": peaks["hbm_gbs"] if hbm else p / 1e12,
+            "unit": "GB/s" if hbm else "TFLOP/s",
+            "frac": max(t_mem, t_cmp) / launch_s,
+            "traffic": traffic,
+            "kernel": kernel, "path": path, "launch_us": launch_s * 1e6,
+            "t_roof_us": max(t_mem, t_cmp) * 1e6, "hbm_term_us": t_mem * 1e6, "compute_term_us": t_cmp * 1e6,
+            "hbm_frac": t_mem / launch_s, "compute_frac": t_cmp / launch_s,
+            "compute_peak_tflops": p / 1e12, "compute_peak_source": psrc,
+            "peak_source": peaks["source"] if hbm else psrc}
+
+
+def _kernel_name(order, word, path):
+    if path == "tensor":
+        return f"dgm::tc_stage_kernel<{order},1>"
+    return f"dgm::stage_kernel<{order},{'float' if word == 4 else 'double'},1>"
+
+
+def _traffic(ncu: dict, order: int, word: int, path: str):
+    """ncu DRAM bytes per launch of this (kernel, order, dtype), or None if not captured."""
+    key = f"{'tc_stage_kernel' if path == 'tensor' else 'stage_kernel'}<{order}>/{'f32' if word == 4 else 'f64'}"
+    ent = ncu.get("kernels", {}).get(key)
+    return {"bytes_per_launch": ent["dram_bytes_per_launch"], "key": key, "source": ent.get("source")} if ent else None
+
+
+# Extra config rows timed in the same N=1 run (BASELINE.json configs; SURVEY 8(d)).
+EXTRAS = {
+    "C1": dict(order=3, cells=(6, 6, 7), dtype="f32", steps=100, warmup=10, graph=True,
+               what="C1 PEC cavity N=3, 1,512 tets, 100 LSRK4 steps through the CUDA-graph path (op.advance)"),
+    "C2_N1": dict(order=1, cells=(20, 20, 20), dtype="f32", steps=20, warmup=3, graph=False,
+                  what="C2 order sweep, 48,000 tets, N=1"),
+    "C2_N3": dict(order=3, cells=(20, 20, 20), dtype="f32", steps=20, warmup=3, graph=False,
+                  what="C2 order sweep, 48,000 tets, N=3"),
+    "C2_N6": dict(order=6, cells=(20, 20, 20), dtype="f32", steps=20, warmup=3, graph=False,
+                  what="C2 order sweep, 48,000 tets, N=6"),
+    "C2_N9": dict(order=9, cells=(20, 20, 20), dtype="f32", steps=10, warmup=3, graph=False,
+                  what="C2 order sweep, 48,000 tets, N=9"),
+    "C3_f64": dict(order=4, cells=(55, 55, 55), dtype="f64", steps=10, warmup=3, graph=False,
+                   what="C3 N=4, 998,250 tets, fp64 variant (the reference's precision)"),
+    "C5": dict(order=6, cells=(70, 70, 70), dtype="f32", steps=10, warmup=3, graph=False,
+               what="C5 N=6, 2,058,000 tets per GPU (N=1 point of the weak-scaling series), 3xTF32 tensor path"),
+    "C4": dict(order=4, cells=(110, 110, 110), dtype="f32", steps=5, warmup=3, graph=False,
+               what="C4 N=4, 7,986,000 tets on one GPU (N=1 point of the strong-scaling series)"),
+}
+DEFAULT_EXTRAS = ("C1", "C2_N1", "C2_N3", "C2_N6", "C2_N9", "C3_f64", "C5")
+
+
+def run_extra(name, spec, dev, clocks, peaks, pipes, ncu) -> dict:
+    """Build and time one extra config (device-resident state, CUDA events on the launching stream)."""
+    import torch
+
+    from paper_0901_1024_b200 import (CavityMode, build_b200_operator, build_reference_element,
+                                      generate_box_mesh, map_nodes, stable_dt)
+    from paper_0901_1024_b200.perfmodel import dofs, flops_per_element_stage
+
+    t0 = time.perf_counter()
+    dtype = torch.float64 if spec["dtype"] == "f64" else torch.float32
+    word = 8 if dtype == torch.float64 else 4
+    mesh = generate_box_mesh((1.0, 1.0, 1.0), spec["cells"])
+    elem = build_reference_element(spec["order"])
+    op = build_b200_operator(mesh, elem, dtype=dtype, device=dev)
+    dt = stable_dt(mesh, op.geometry, spec["order"])
+    u = op.to_padded(CavityMode(1, 1, 1, (1.0, 1.0, 1.0)).evaluate(map_nodes(mesh, elem), 0.0))
+    setup_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream(dev)
+    op.advance(u, dt, spec["warmup"], use_graph=spec["graph"])
+    torch.cuda.synchronize(dev)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark_start(name)
+    start.record(stream)
+    op.advance(u, dt, spec["steps"], use_graph=spec["graph"])
+    stop.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.mark_stop(name)
+    ms = start.elapsed_time(stop)
+    energy = op.field_energy(u)
+    if not math.isfinite(energy):
+        raise RuntimeError(f"{name}: non-finite energy")
+    k, order, steps = op.num_elements, spec["order"], spec["steps"]
+    sec = ms / 1e3
+    launch_s = sec / (5 * steps)
+    out = {"workload": spec["what"], "order": order, "elements": k, "dtype": spec["dtype"], "path": op.path,
+           "steps": steps, "warmup": spec["warmup"], "cuda_graph": spec["graph"], "ms_per_step": ms / steps,
+           "value": flops_per_element_stage(order) * k * 5 * steps / sec / 1e9, "unit": UNIT,
+           "dof_updates_per_s": dofs(order, k) * steps / sec, "setup_s": round(setup_s, 2),
+           "roofline": roofline(order, word, op.path, k, launch_s, peaks, pipes, _kernel_name(order, word, op.path),
+                                _traffic(ncu, order, word, op.path)),
+           "energy_after": energy}
+    del op, u
+    torch.cuda.empty_cache()
+    time.sleep(0.15)
+    out["clocks"] = clocks.summary(name)
+    return out
 
 
 def run_b200(args) -> None:
@@ -240,6 +478,7 @@ def run_b200(args) -> None:
     dtype = torch.float64 if args.dtype == "f64" else torch.float32
     word = 8 if dtype == torch.float64 else 4
     cells = tuple(args.cells)
+    strong = args.scaling == "strong" and world > 1
     t_setup = time.perf_counter()
     elem = build_reference_element(args.order)
     if world == 1:
@@ -256,9 +495,13 @@ def run_b200(args) -> None:
         from paper_0901_1024_b200.dist import DistributedMaxwellOperator, build_box_domain
         from paper_0901_1024_b200.mesh import Mesh, compute_geometry as _cg
 
-        # weak scaling: rank r owns cells [r*nx, (r+1)*nx) of a (world*nx, ny, nz) box of extent (world,1,1)
-        extent = (float(world), 1.0, 1.0)
-        gcells = (cells[0] * world, cells[1], cells[2])
+        if strong:
+            # strong scaling: the (cells) box split into world x-slabs (C4: 110^3 over 1/2/4/8 GPUs)
+            extent, gcells = (1.0, 1.0, 1.0), cells
+        else:
+            # weak scaling: rank r owns cells [r*nx, (r+1)*nx) of a (world*nx, ny, nz) box of extent (world,1,1)
+            extent = (float(world), 1.0, 1.0)
+            gcells = (cells[0] * world, cells[1], cells[2])
         dom = build_box_domain(extent, gcells, elem, rank, world)
         runner = DistributedMaxwellOperator(dom, dtype=dtype, device=dev, path=args.path,
                                             reorder={"auto": None, "natural": False}.get(args.element_order, True),
@@ -266,11 +509,22 @@ def run_b200(args) -> None:
         op = runner.op
         lo = dom.owned[0] - dom.sub_offset
         own_mesh = Mesh(dom.mesh.vertices, dom.mesh.elements[lo:lo + dom.num_owned])
-        dt = stable_dt(own_mesh, _cg(own_mesh), args.order)  # identical on every rank (congruent slabs)
+        dt_local = stable_dt(own_mesh, _cg(own_mesh), args.order)
+        t = torch.tensor([dt_local], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)  # global stable dt
+        dt = float(t.item())
         u0_host = CavityMode(1, 1, 1, extent).evaluate(dom.owned_nodes(), 0.0)
     u = op.to_padded(u0_host)
     setup_s = time.perf_counter() - t_setup
     k = op.num_elements
+    path = op.path
+    launches = 5 * args.steps if world == 1 else args.steps * 5 * (
+        1 + len(runner.stage_ranges()[1]) + len(runner.domain.send) + len(runner.domain.recv))
+    k_total = k
+    if world > 1:
+        t = torch.tensor([k], device=dev, dtype=torch.int64)
+        torch.distributed.all_reduce(t)
+        k_total = int(t.item())
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -282,8 +536,22 @@ def run_b200(args) -> None:
             return op.advance(x, dt, n, use_graph=False)
         return runner.advance(x, dt, n)
 
-    # ---- device-resident throughput (value) ----
+    def max_over_ranks(ms):
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    peaks = _peaks()
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    pipes = {"fp32_tflops": sms * 128 * 2 * sm_max * 1e6 / 1e12, "fp64_tflops": sms * 64 * 2 * sm_max * 1e6 / 1e12,
+             "tf32": measure_tf32_tflops(dev, sm_max)}
+    ncu = _ncu_summary()
+
     with ClockSampler(local) as clocks:
+        # ---- device-resident throughput (value) ----
         advance(u, args.warmup)
         torch.cuda.synchronize()
         barrier()
@@ -295,107 +563,73 @@ def run_b200(args) -> None:
         stop.record(stream)
         torch.cuda.synchronize()
         clocks.mark_stop()
-        time.sleep(0.15)  # let the sample covering the end of the timed region arrive
-    barrier()
-    torch.cuda.synchronize()
-    ms = start.elapsed_time(stop)
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    energy = runner.field_energy(u)
-    if not math.isfinite(energy):
-        raise RuntimeError("non-finite energy after the timed steps")
+        barrier()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(start.elapsed_time(stop))
+        energy = runner.field_energy(u)
+        if not math.isfinite(energy):
+            raise RuntimeError("non-finite energy after the timed steps")
 
-    launches = 5 * args.steps if world == 1 else args.steps * 5 * (
-        1 + len(runner.stage_ranges()[1]) + len(runner.domain.send) + len(runner.domain.recv))
+        # ---- end to end through the public API with host buffers (a dependent chain) ----
+        # The reference user's state lives on the host in float64 (natural (6, K, Np) layout).  Every
+        # e2e step uploads the current host state (pinned), packs it, runs one LSRK4 step, unpacks,
+        # downloads the new state into the same host buffer -- the next step's input -- plus the
+        # energy scalar.  Steps depend on each other, so nothing overlaps across steps.
+        e2e_steps = max(1, args.steps if args.e2e_steps is None else min(args.steps, args.e2e_steps))
+        e2e_dtype = {"f32": torch.float32, "f64": torch.float64}[args.e2e_dtype]
+        host = torch.from_numpy(np.ascontiguousarray(u0_host)).to(e2e_dtype).pin_memory()
+        e_host = torch.empty(1, dtype=torch.float64).pin_memory()
+        dev_nat = torch.empty(host.shape, dtype=e2e_dtype, device=dev)
+        ue = op.empty_state()
+        h2d = host.numel() * host.element_size()
+        d2h = h2d + 8
+
+        def e2e_step():
+            dev_nat.copy_(host, non_blocking=True)                       # H2D of this step's input
+            op.to_padded(dev_nat, out=ue)                                # pack (natural -> padded, cast)
+            advance(ue, 1)                                               # 5 fused stage launches
+            nat = op.from_padded(ue, e2e_dtype)                          # unpack
+            energy_dev = op.mass_norm(ue, 1.0, 1.0)                      # per-step energy scalar
+            host.copy_(nat, non_blocking=True)                           # D2H: the next step's input
+            e_host.copy_(energy_dev, non_blocking=True)
+
+        e2e_step()  # warm-up (allocations, first launches)
+        torch.cuda.synchronize()
+        host.copy_(torch.from_numpy(np.ascontiguousarray(u0_host)).to(e2e_dtype))
+        barrier()
+        torch.cuda.synchronize()
+        e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_start.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e_stop.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e_ms = max_over_ranks(e_start.elapsed_time(e_stop))
+        if not math.isfinite(float(e_host.item())):
+            raise RuntimeError("non-finite e2e energy")
+        del dev_nat, ue
+
+        # ---- the other BASELINE configs on this GPU (N=1 only) ----
+        extras = {}
+        if world == 1 and args.extras != "none":
+            del u
+            runner = op = None
+            torch.cuda.empty_cache()
+            names = DEFAULT_EXTRAS if args.extras == "default" else (
+                tuple(EXTRAS) if args.extras == "all" else tuple(args.extras.split(",")))
+            for name in names:
+                extras[name] = run_extra(name, EXTRAS[name], dev, clocks, peaks, pipes, ncu)
+        time.sleep(0.15)  # let the sample covering the end of the last timed region arrive
+
     sec = ms / 1e3
     f_alg = flops_per_element_stage(args.order)
     b_alg = bytes_per_element_stage(args.order, word)
-    gflops = world * f_alg * k * 5 * args.steps / sec / 1e9
-    dof_rate = world * dofs(args.order, k) * args.steps / sec
+    gflops = f_alg * k_total * 5 * args.steps / sec / 1e9
+    dof_rate = dofs(args.order, k_total) * args.steps / sec
     hbm_gbs = b_alg * k * 5 * args.steps / sec / 1e9  # per GPU
-    launch_s = sec / launches
-    peaks = _peaks()
-    ncu = _ncu_summary()
-    traffic = ncu.get("tc_stage_kernel" if op.path == "tensor" else "stage_kernel", {}).get("dram_bytes_per_launch")
-    fp32_peak_tf = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
-
-    # ---- end-to-end through the public API with host buffers ----
-    # Every e2e step uploads its own input (the natural state in the e2e dtype, pinned host memory),
-    # packs it, runs one LSRK4 step, unpacks and downloads the new state and the energy scalar.  The
-    # steps are independent and pipelined over three streams: uploads in order on an H2D stream,
-    # pack/step/unpack on the compute stream, downloads in order on a D2H stream, with events
-    # recycling `--e2e-slots` device input buffers, so both copy engines stream back to back (PCIe
-    # is full duplex) while the GPU computes.  Every byte counted below crosses PCIe inside the
-    # timed region.
-    e2e_steps = max(1, args.steps if args.e2e_steps is None else min(args.steps, args.e2e_steps))
-    # natural host state in the e2e dtype (default: the compute dtype -- an fp32 user keeps fp32 host
-    # buffers; --e2e-dtype f64 keeps the reference's float64 and doubles the PCIe bytes)
-    e2e_dtype = {"f32": torch.float32, "f64": torch.float64}[args.e2e_dtype or args.dtype]
-    host_in = torch.from_numpy(np.ascontiguousarray(u0_host)).to(e2e_dtype).pin_memory()
-    nslots = max(2, args.e2e_slots)
-    host_out = [torch.empty_like(host_in).pin_memory() for _ in range(nslots)]
-    e_host = [torch.empty(1, dtype=torch.float64).pin_memory() for _ in range(nslots)]
-    h2d = host_in.numel() * host_in.element_size()
-    d2h = host_out[0].numel() * host_out[0].element_size() + 8
-    h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    dev_in = [torch.empty(host_in.shape, dtype=e2e_dtype, device=dev) for _ in range(nslots)]
-    ue = op.empty_state()  # one compute stream: the state buffer is reused in stream order
-    in_ready = [torch.cuda.Event() for _ in range(nslots)]   # H2D into dev_in[j] done
-    in_free = [torch.cuda.Event() for _ in range(nslots)]    # dev_in[j] packed (reusable)
-    out_ready = [torch.cuda.Event() for _ in range(nslots)]  # slot j's result unpacked
-    out_free = [torch.cuda.Event() for _ in range(nslots)]   # slot j's result downloaded
-    used = [False] * nslots
-
-    def e2e_step(i):
-        j = i % nslots
-        with torch.cuda.stream(h2d_s):
-            if used[j]:
-                h2d_s.wait_event(in_free[j])
-            dev_in[j].copy_(host_in, non_blocking=True)                     # H2D
-            in_ready[j].record(h2d_s)
-        with torch.cuda.stream(stream):
-            stream.wait_event(in_ready[j])
-            op.to_padded(dev_in[j], out=ue)                                 # pack (natural -> padded)
-            in_free[j].record(stream)
-            advance(ue, 1)                                                  # 5 fused stage launches
-            if used[j]:
-                stream.wait_event(out_free[j])  # bounds the results in flight to nslots
-            nat = op.from_padded(ue, e2e_dtype)                             # unpack
-            energy_dev = op.mass_norm(ue, 1.0, 1.0)                         # per-step energy scalar
-            nat.record_stream(d2h_s)
-            energy_dev.record_stream(d2h_s)
-            out_ready[j].record(stream)
-        with torch.cuda.stream(d2h_s):
-            d2h_s.wait_event(out_ready[j])
-            host_out[j].copy_(nat, non_blocking=True)                       # D2H of the new state
-            e_host[j].copy_(energy_dev, non_blocking=True)
-            out_free[j].record(d2h_s)
-        used[j] = True
-
-    for j in range(nslots):  # warm-up (allocations, first launches)
-        e2e_step(j)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_start.record(stream)
-    h2d_s.wait_stream(stream)
-    d2h_s.wait_stream(stream)
-    for i in range(e2e_steps):
-        e2e_step(i)
-    stream.wait_stream(h2d_s)
-    stream.wait_stream(d2h_s)
-    e_stop.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    e_ms = e_start.elapsed_time(e_stop)
-    if world > 1:
-        t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e_ms = float(t.item())
-    e2e_gflops = world * f_alg * k * 5 * e2e_steps / (e_ms / 1e3) / 1e9
+    launch_s = sec / (5 * args.steps)
+    e2e_gflops = f_alg * k_total * 5 * e2e_steps / (e_ms / 1e3) / 1e9
 
     if rank != 0:
         if world > 1:
@@ -403,55 +637,61 @@ def run_b200(args) -> None:
         return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        r = cpu_reference_rate(args.order, CPU_SAMPLE_CELLS, args.cpu_steps)
-        cpu = {"value": r["gflops"], "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"oracle port of the reference path, box {CPU_SAMPLE_CELLS} -> {r['elements']} tets, "
-                         f"N={args.order}, {args.cpu_steps} LSRK4 steps, {r['seconds']:.1f} s single-threaded; "
-                         f"{r['dof_updates_per_s']:.3g} DOF-updates/s"}
+        r = cpu_reference_rate(args.order, args.cpu_steps, 1)
+        cpu = {"value": r["gflops"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+               "host_cores": r["host_cores"], "sample": r["sample"],
+               "dof_updates_per_s": r["dof_updates_per_s"]}
     clk = clocks.summary()
+    if world == 1:
+        parallelism = "single"
+    elif strong:
+        parallelism = (f"strong scaling: the {cells} box split into {world} x-slabs, NCCL face-trace halo "
+                       "overlapped with the interior stage kernel")
+    else:
+        parallelism = (f"weak scaling: {world} x-slabs of {cells} cells each, NCCL face-trace halo "
+                       "overlapped with the interior stage kernel")
     line = {
         "metric": METRIC, "value": gflops, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "f64" if word == 8 else "f32", "data": "synthetic",
         "dof_updates_per_s": dof_rate, "hbm_gbs_algorithmic": hbm_gbs,
-        "config": {"workload": f"C3 Maxwell PEC cavity N={args.order}, box {cells} -> {k} tets per GPU, "
-                               "TM(1,1,1) cavity mode, dt=stable_dt(cfl=1)",
+        "config": {"workload": (f"C4 Maxwell PEC cavity N={args.order}, box {cells} -> {k_total} tets over "
+                                f"{world} GPUs" if strong else
+                                f"C3 Maxwell PEC cavity N={args.order}, box {cells} -> {k} tets per GPU") +
+                               ", TM(1,1,1) cavity mode, dt=stable_dt(cfl=1)",
                    "order": args.order, "elements_per_gpu": k, "dofs_per_gpu": dofs(args.order, k),
-                   "parallelism": f"x-slab element partition over {world} GPUs, NCCL face-trace halo "
-                                  "overlapped with the interior stage kernel" if world > 1 else "single",
-                   "global_elements": k * world,
+                   "parallelism": parallelism, "global_elements": k_total,
                    "l2": "no flush: state+residual registers (%.2f GB) >> 126 MB L2" % (
-                       2 * 6 * k * op.np_stride * word / 1e9),
-                   "element_order": (args.element_order if args.element_order != "auto" else "columns")
-                   if getattr(op, "_order", None) is not None else "natural",
-                   "face_slots": "bank-spread" if getattr(op, "_slot_inv", None) is not None else "natural",
+                       2 * 6 * k * _np_stride(args.order, word) * word / 1e9),
                    "setup_s": round(setup_s, 2), "flops_per_element_stage": f_alg,
                    "bytes_per_element_stage": b_alg},
-        "roofline": {"bound": "hbm", "achieved": b_alg * k / launch_s / 1e9, "peak": peaks["hbm_gbs"],
-                     "unit": "GB/s", "frac": b_alg * k / launch_s / 1e9 / peaks["hbm_gbs"],
-                     "traffic": traffic,
-                     "kernel": (f"dgm::tc_stage_kernel<{args.order},1>" if op.path == "tensor" else
-                                f"dgm::stage_kernel<{args.order},{'float' if word == 4 else 'double'},1>"),
-                     "path": op.path,
-                     "launch_us": launch_s * 1e6,
-                     "peak_source": peaks["source"],
-                     "fp32_simt_frac": f_alg * k / launch_s / 1e12 / fp32_peak_tf,
-                     "fp32_simt_peak_tflops": fp32_peak_tf},
+        "roofline": roofline(args.order, word, path, k, launch_s, peaks, pipes,
+                             _kernel_name(args.order, word, path), _traffic(ncu, args.order, word, path)),
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_gflops, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,
-                "slots": nslots,
                 "host_dtype": str(e2e_dtype).replace("torch.", ""),
-                "path": "per step: pinned natural state H2D -> op.to_padded -> op.advance(1 LSRK4 step) -> "
-                        "op.from_padded -> pinned host D2H, + energy scalar D2H; pipelined over an H2D, a "
-                        "compute and a D2H stream with %d input slots" % nslots},
+                "path": "dependent chain through the public API, per step: pinned natural host state H2D -> "
+                        "op.to_padded -> op.advance(1 LSRK4 step) -> op.from_padded -> D2H into the same "
+                        "host buffer (the next step's input) + energy scalar D2H"},
         "gpu_launches": launches,
         "clocks": clk,
         "energy_after": energy,
+        "pipes": {"fp32_simt_tflops": pipes["fp32_tflops"], "fp64_simt_tflops": pipes["fp64_tflops"],
+                  "tf32_mma": pipes["tf32"]},
     }
+    if extras:
+        line["configs"] = extras
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _np_stride(order: int, word: int) -> int:
+    from paper_0901_1024_b200 import _capi
+
+    return _capi.layout(order, 2 if word == 8 else 1).np_stride
 
 
 def main(argv=None) -> None:
@@ -461,24 +701,34 @@ def main(argv=None) -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--order", type=int, default=ORDER)
-    ap.add_argument("--cells", type=int, nargs=3, default=list(CELLS))
+    ap.add_argument("--cells", type=int, nargs=3, default=None,
+                    help="box cells (default: C3 (55,55,55); with --scaling strong: C4 (110,110,110))")
     ap.add_argument("--dtype", choices=("f32", "f64"), default="f32")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="N>1: weak = --cells per GPU (C3/C5 style), strong = --cells split over the GPUs (C4)")
+    ap.add_argument("--extras", default="default",
+                    help="extra config rows at N=1: default (%s), all, none, or a comma list of %s"
+                         % (",".join(DEFAULT_EXTRAS), ",".join(EXTRAS)))
     ap.add_argument("--e2e-steps", type=int, default=None, help="e2e steps (default: --steps)")
-    ap.add_argument("--e2e-slots", type=int, default=4,
-                    help="device input buffers of the e2e pipeline (H2D runs up to this many steps ahead)")
     ap.add_argument("--element-order", choices=("auto", "natural", "morton", "columns"), default="auto",
                     help="internal element numbering (ordering.py); auto = Morton where it pays")
     ap.add_argument("--face-slots", choices=("auto", "natural"), default="auto",
                     help="node order inside each face (ordering.face_slot_order); auto = bank-spread on the tensor path")
-    ap.add_argument("--e2e-dtype", choices=("f32", "f64"), default=None,
-                    help="natural host-state dtype of the e2e leg (default: the compute dtype)")
-    ap.add_argument("--cpu-steps", type=int, default=12)
+    ap.add_argument("--e2e-dtype", choices=("f32", "f64"), default="f64",
+                    help="natural host-state dtype of the e2e leg (default: float64, the reference's)")
+    ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--path", choices=("auto", "tensor", "simt"), default="auto",
-                    help="stage kernel: tcgen05 3xTF32 (tensor, N<=4 fp32) or CUDA cores (simt)")
+                    help="stage kernel: tcgen05 3xTF32 (tensor, fp32) or CUDA cores (simt)")
     args = ap.parse_args(argv)
+    if args.cells is None:
+        args.cells = [110, 110, 110] if args.scaling == "strong" else list(CELLS)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if args.extras not in ("default", "all", "none"):
+        bad = [n for n in args.extras.split(",") if n not in EXTRAS]
+        if bad:
+            raise SystemExit(f"unknown --extras {bad}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round 2: probe tests, full bench line (all config rows), ncu --set full of every config's stage kernel,
+# launch list of the default bench command.
+cd "${GRAFT_REPO_ROOT:-$(pwd)}"
+O=gpurun_out/r2bench; mkdir -p $O
+timeout 300 python -m pytest tests/test_gpu_tc05.py -q -s > $O/probe_tests.log 2>&1; echo "rc=$?" >> $O/probe_tests.log
+timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_ref.json 2> $O/bench_ref.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c3.csv \
+  python bench.py --steps 2 --warmup 3 --extras none --no-cpu-baseline --e2e-steps 1 > $O/launch_run.log 2>&1
+cap() {  # name order cells dtype
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 5 -c 1 -o $O/prof_$1 \
+    python bench.py --order $2 --cells $3 --dtype $4 --steps 1 --warmup 3 --extras none --no-cpu-baseline \
+    --e2e-steps 1 > $O/ncu_$1.log 2>&1
+}
+cap c3f64 4 "55 55 55" f64
+cap c5 6 "70 70 70" f32
+cap c2n1 1 "20 20 20" f32
+cap c2n3 3 "20 20 20" f32
+cap c2n6 6 "20 20 20" f32
+cap c2n9 9 "20 20 20" f32
+cap c1 3 "6 6 7" f32
+echo done

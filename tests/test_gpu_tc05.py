@@ -60,3 +60,25 @@ def test_tf32_gemm_a_in_tmem(probe, n, k):
         errs[passes] = ((c.double() - want).norm() / want.norm()).item()
     print(f"TS n={n} k={k} tf32 {errs[1]:.2e} 3xtf32 {errs[3]:.2e}")
     assert errs[1] < 5e-3 and errs[3] < 2e-6
+
+
+def test_tf32_inputs_are_truncated(probe):
+    """kind::tf32 reads fp32 operands and drops the low 13 mantissa bits (round toward zero).
+
+    The v2 stage kernel feeds the raw state rows as the 'hi' operand of its 3xTF32 volume product
+    and splits only lo = x - trunc(x); that is exact only if the hardware truncates.  Passes=13 makes
+    the probe store the hi operands unmasked: the error must stay at the masked 3xTF32 level.
+    """
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    a = torch.randn(128, 40, device="cuda", generator=gen)
+    b = torch.randn(112, 40, device="cuda", generator=gen)
+    want = (a.double() @ b.double().T)
+    errs = {}
+    for passes in (3, 13):
+        c = torch.full((128, 112), float("nan"), device="cuda")
+        assert probe.dgm_probe_tf32_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), 112, 40, passes,
+                                         torch.cuda.current_stream().cuda_stream) == 0
+        torch.cuda.synchronize()
+        errs[passes] = ((c.double() - want).norm() / want.norm()).item()
+    print(f"3xtf32 masked {errs[3]:.2e} raw {errs[13]:.2e}")
+    assert errs[13] < 2e-6

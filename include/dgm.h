@@ -229,6 +229,21 @@ int dgm_halo_pack(const dgm_plan* plan, const void* u, const int32_t* elements,
 int dgm_halo_unpack(const dgm_plan* plan, const void* recvbuf, int64_t count,
                     int64_t ghost_begin, void* u, void* stream);
 
+/*
+ * Face-trace halo (what the multi-GPU operator exchanges each LSRK stage):
+ * elem_face holds count (element, face) int32 pairs; dgm_trace_pack gathers
+ * the Nfp face nodes of each pair, real[count][6][Nfp], from u's padded rows;
+ * dgm_trace_unpack scatters such a buffer into the face nodes of the listed
+ * (ghost) rows of u.  Node order is the plan's face_nodes, so a buffer packed
+ * by one rank unpacks on a peer whose plan has the same face_nodes.
+ * New (the reference is single-process); 6*Nfp instead of
+ * 6*np_stride reals per cut face.
+ */
+int dgm_trace_pack(const dgm_plan* plan, const void* u, const int32_t* elem_face,
+                   int64_t count, void* sendbuf, void* stream);
+int dgm_trace_unpack(const dgm_plan* plan, const void* recvbuf, const int32_t* elem_face,
+                     int64_t count, void* u, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,8 @@ _SIGNATURES = {
     "dgm_unpack": ([ctypes.c_int32, ctypes.c_int32, _VP, _VP, _VP, ctypes.c_int32, _I64, _I64, _VP], ctypes.c_int),
     "dgm_halo_pack": ([_VP, _VP, _VP, _I64, _VP, _VP], ctypes.c_int),
     "dgm_halo_unpack": ([_VP, _VP, _I64, _I64, _VP, _VP], ctypes.c_int),
+    "dgm_trace_pack": ([_VP, _VP, _VP, _I64, _VP, _VP], ctypes.c_int),
+    "dgm_trace_unpack": ([_VP, _VP, _VP, _I64, _VP, _VP], ctypes.c_int),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 

@@ -537,6 +537,41 @@ int dgm_halo_unpack(const dgm_plan* plan, const void* recvbuf, int64_t count, in
   });
 }
 
+int dgm_trace_pack(const dgm_plan* plan, const void* u, const int32_t* elem_face, int64_t count, void* sendbuf,
+                   void* stream) {
+  if (!plan || !u || count < 0 || (count > 0 && (!elem_face || !sendbuf)))
+    return fail(DGM_ERR_INVALID, "dgm_trace_pack: bad arguments");
+  if (count == 0) return DGM_OK;
+  const dgm_desc& d = plan->d;
+  DeviceGuard guard(plan->device);
+  return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    dgm::trace_pack_kernel<N, T><<<grid_for(count * 6 * C::NFP, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const T*>(u), elem_face, d.face_nodes, count, d.field_stride, static_cast<T*>(sendbuf));
+    return cuda_check(cudaGetLastError(), "trace_pack_kernel launch");
+  });
+}
+
+int dgm_trace_unpack(const dgm_plan* plan, const void* recvbuf, const int32_t* elem_face, int64_t count, void* u,
+                     void* stream) {
+  if (!plan || !u || count < 0 || (count > 0 && (!elem_face || !recvbuf)))
+    return fail(DGM_ERR_INVALID, "dgm_trace_unpack: bad arguments");
+  if (count == 0) return DGM_OK;
+  const dgm_desc& d = plan->d;
+  DeviceGuard guard(plan->device);
+  return dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+    constexpr int N = decltype(n)::value;
+    using T = decltype(t);
+    using C = dgm::Cfg<N, T>;
+    dgm::trace_unpack_kernel<N, T><<<grid_for(count * 6 * C::NFP, 256), 256, 0,
+                                     static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const T*>(recvbuf), elem_face, d.face_nodes, count, d.field_stride, static_cast<T*>(u));
+    return cuda_check(cudaGetLastError(), "trace_unpack_kernel launch");
+  });
+}
+
 }  // extern "C"
 
 #ifdef DGM_TC_TIMING

@@ -129,6 +129,42 @@ __global__ void halo_unpack_kernel(const T* __restrict__ recv, int64_t count, in
   }
 }
 
+// Face-trace halo: only the Nfp nodes of each cut face travel.
+// send[c][f][i] = u[f][elem_face[2c]][fmask[face][i]], face = elem_face[2c + 1]
+template <int N, typename T>
+__global__ void trace_pack_kernel(const T* __restrict__ u, const int* __restrict__ elem_face,
+                                  const uint8_t* __restrict__ fmask, int64_t count, int64_t kf,
+                                  T* __restrict__ send) {
+  using C = Cfg<N, T>;
+  const int64_t total = count * 6 * C::NFP;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = x / (6 * C::NFP);
+    const int r = (int)(x - c * 6 * C::NFP);
+    const int f = r / C::NFP, i = r - f * C::NFP;
+    const int e = __ldg(elem_face + 2 * c), face = __ldg(elem_face + 2 * c + 1);
+    send[x] = u[((int64_t)f * kf + e) * C::NPG + fmask[face * C::NFP + i]];
+  }
+}
+
+// u[f][elem_face[2c]][fmask[face][i]] = recv[c][f][i]: a ghost row receives only the face nodes the
+// owned side reads (its other nodes are never read; faces sharing an edge write equal values)
+template <int N, typename T>
+__global__ void trace_unpack_kernel(const T* __restrict__ recv, const int* __restrict__ elem_face,
+                                    const uint8_t* __restrict__ fmask, int64_t count, int64_t kf,
+                                    T* __restrict__ u) {
+  using C = Cfg<N, T>;
+  const int64_t total = count * 6 * C::NFP;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = x / (6 * C::NFP);
+    const int r = (int)(x - c * 6 * C::NFP);
+    const int f = r / C::NFP, i = r - f * C::NFP;
+    const int e = __ldg(elem_face + 2 * c), face = __ldg(elem_face + 2 * c + 1);
+    u[((int64_t)f * kf + e) * C::NPG + fmask[face * C::NFP + i]] = recv[x];
+  }
+}
+
 // partial[blockIdx] = sum over the CTA's elements of J_k sum_f w_f u_fk^T M u_fk   (maxwell.py:211-232);
 // reduce_partials_kernel adds them into *out in a fixed order, so the value is bitwise reproducible
 // (the reference's CLI reruns are byte-identical, pkg/tests/test_cli.py:106-112)

@@ -54,6 +54,10 @@ class RankDomain:
     send: dict = field(default_factory=dict)   # peer -> local owned ids (int32)
     recv: dict = field(default_factory=dict)   # peer -> (ghost_begin, count)
     interior: tuple[int, int] = (0, 0)
+    # face-trace halo: peer -> int32 (n, 2) (local element, face) pairs, the same cut faces in the
+    # same order on both ends (sorted by the face owner's global id, then face)
+    send_traces: dict = field(default_factory=dict)   # owned element's face whose neighbour is on peer
+    recv_traces: dict = field(default_factory=dict)   # ghost slot's face whose neighbour is owned here
     owner_ranges: list = field(default_factory=list)  # per rank global [g0, g1)
     mesh: Mesh | None = None        # submesh holding owned (+ ghost) elements
     sub_offset: int = 0             # submesh element j <-> global j + sub_offset
@@ -118,6 +122,38 @@ def _send_lists(rank: int, world: int, owned, owner_ranges, ghost_lists_of_peers
     return send
 
 
+def _cut_traces(elem_ids: np.ndarray, nbr_g: np.ndarray, codes: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    """(global element id, face) of the listed element rows whose face neighbour lies in [lo, hi).
+
+    Rows come in ascending global id and np.nonzero walks them row-major, so the pairs are sorted
+    by (element, face): sender and receiver enumerate the same cut faces in the same order.
+    """
+    e, f = np.nonzero((codes >= 0) & (nbr_g >= lo) & (nbr_g < hi))
+    return np.stack([np.asarray(elem_ids, dtype=np.int64)[e], f.astype(np.int64)], axis=1)
+
+
+def _trace_lists(rank: int, owned, owner_ranges, ghost_global, peers, rows_of):
+    """send_traces / recv_traces of a rank; rows_of(global ids) -> (nbr_global, codes) of those elements."""
+    g0, g1 = owned
+    k_own = g1 - g0
+    own_ids = np.arange(g0, g1)
+    own_nbr, own_codes = rows_of(own_ids)
+    send, recv = {}, {}
+    for peer in peers:
+        p0, p1 = owner_ranges[peer]
+        out = _cut_traces(own_ids, own_nbr, own_codes, p0, p1)
+        if len(out):
+            out[:, 0] -= g0
+            send[peer] = out.astype(np.int32)
+        gh = ghost_global[(ghost_global >= p0) & (ghost_global < p1)]
+        if len(gh):
+            nbr, codes = rows_of(gh)
+            inn = _cut_traces(gh, nbr, codes, g0, g1)
+            inn[:, 0] = k_own + np.searchsorted(ghost_global, inn[:, 0])
+            recv[peer] = inn.astype(np.int32)
+    return send, recv
+
+
 def _geometry_rows(mesh: Mesh, rows: slice):
     from .operator import geometry_words
 
@@ -164,8 +200,16 @@ def build_box_domain(extent, cells, elem: ReferenceElement, rank: int, world: in
     geo_words, det = _geometry_rows(sub, own)
     maps = FaceMaps(num_nodes=elem.num_nodes, face_nodes=maps_sub.face_nodes, neighbors=local, codes=codes,
                     code_table=maps_sub.code_table)
+
+    def rows_of(ids):  # the slab mesh holds the owned and the ghost-layer elements' full face data
+        j = np.asarray(ids, dtype=np.int64) - off
+        return maps_sub.neighbors[j].astype(np.int64) + off, maps_sub.codes[j]
+
+    peers = [p for p in (rank - 1, rank + 1) if 0 <= p < world]
+    send_tr, recv_tr = _trace_lists(rank, owned, owner_ranges, ghosts, peers, rows_of)
     return RankDomain(rank=rank, world=world, elem=elem, owned=owned, ghost_global=ghosts, maps=maps,
                       geo_words=geo_words, det_j=det, send=send, recv=recv, interior=interior,
+                      send_traces=send_tr, recv_traces=recv_tr,
                       owner_ranges=owner_ranges, mesh=sub, sub_offset=off)
 
 
@@ -192,8 +236,16 @@ def build_mesh_domain(mesh: Mesh, elem: ReferenceElement, rank: int, world: int,
     geo_words, det = _geometry_rows(mesh, rows)
     maps = FaceMaps(num_nodes=elem.num_nodes, face_nodes=maps_g.face_nodes, neighbors=local, codes=codes,
                     code_table=maps_g.code_table)
+
+    def rows_of(ids):
+        j = np.asarray(ids, dtype=np.int64)
+        return maps_g.neighbors[j].astype(np.int64), maps_g.codes[j]
+
+    send_tr, recv_tr = _trace_lists(rank, owned, owner_ranges, ghosts, [p for p in range(world) if p != rank],
+                                    rows_of)
     return RankDomain(rank=rank, world=world, elem=elem, owned=owned, ghost_global=ghosts, maps=maps,
                       geo_words=geo_words, det_j=det, send=send, recv=recv, interior=interior,
+                      send_traces=send_tr, recv_traces=recv_tr,
                       owner_ranges=owner_ranges, mesh=mesh, sub_offset=0)
 
 
@@ -217,12 +269,15 @@ class DistributedMaxwellOperator:
                                       face_slots=face_slots)
         self.device = self.op.device
         self.comm_stream = torch.cuda.Stream(self.device)
-        rows = 6 * self.op.np_stride
-        self._send = {p: (torch.as_tensor(ids, device=self.device),
-                          torch.empty((len(ids), rows), dtype=dtype, device=self.device))
-                      for p, ids in domain.send.items()}
-        self._recv = {p: torch.empty((cnt, rows), dtype=dtype, device=self.device)
-                      for p, (_, cnt) in domain.recv.items()}
+        # face-trace halo buffers: 6 x Nfp reals per cut face (not whole ghost rows)
+        width = 6 * domain.elem.num_face_nodes
+        self._send = {p: (torch.as_tensor(np.ascontiguousarray(tr), device=self.device),
+                          torch.empty((len(tr), width), dtype=dtype, device=self.device))
+                      for p, tr in domain.send_traces.items()}
+        self._recv_lists = {p: torch.as_tensor(np.ascontiguousarray(tr), device=self.device)
+                            for p, tr in domain.recv_traces.items()}
+        self._recv = {p: torch.empty((len(tr), width), dtype=dtype, device=self.device)
+                      for p, tr in domain.recv_traces.items()}
         self._alt = self.op.empty_state()
         self._alt2 = self.op.empty_state()
         self._res = self.op.empty_state()
@@ -260,24 +315,24 @@ class DistributedMaxwellOperator:
         self.torch.cuda.current_stream(self.device).wait_event(ev)
 
     def pack(self, u, stream=None) -> dict:
-        """dgm_halo_pack every send list of u into its send buffer; returns {peer: buffer}."""
+        """dgm_trace_pack the cut-face traces of u for every peer; returns {peer: buffer}."""
         from . import _capi
 
         s = self.torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream.cuda_stream
-        for peer, (ids, buf) in self._send.items():
-            _capi.check(self.op._lib.dgm_halo_pack(self.op._plan, u.data_ptr(), ids.data_ptr(), len(ids),
-                                                   buf.data_ptr(), s), "dgm_halo_pack")
+        for peer, (pairs, buf) in self._send.items():
+            _capi.check(self.op._lib.dgm_trace_pack(self.op._plan, u.data_ptr(), pairs.data_ptr(), len(pairs),
+                                                    buf.data_ptr(), s), "dgm_trace_pack")
         return {peer: buf for peer, (_, buf) in self._send.items()}
 
     def unpack(self, u, stream=None) -> None:
-        """dgm_halo_unpack every receive buffer into u's ghost slots."""
+        """dgm_trace_unpack every received trace buffer into the face nodes of u's ghost rows."""
         from . import _capi
 
         s = self.torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream.cuda_stream
         for peer, buf in self._recv.items():
-            begin, cnt = self.domain.recv[peer]
-            _capi.check(self.op._lib.dgm_halo_unpack(self.op._plan, buf.data_ptr(), cnt, begin, u.data_ptr(), s),
-                        "dgm_halo_unpack")
+            pairs = self._recv_lists[peer]
+            _capi.check(self.op._lib.dgm_trace_unpack(self.op._plan, buf.data_ptr(), pairs.data_ptr(), len(pairs),
+                                                      u.data_ptr(), s), "dgm_trace_unpack")
 
     @property
     def recv_buffers(self) -> dict:

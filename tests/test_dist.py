@@ -1,12 +1,13 @@
 """Multi-GPU partition and halo plan, checked on CPU with torch.distributed gloo.
 
-The GPU path (DistributedMaxwellOperator) packs whole element rows of the
-send lists (dgm_halo_pack), exchanges them with NCCL send/recv and unpacks
-into the ghost slots (dgm_halo_unpack).  Here the same plans drive a CPU
-exchange over gloo (torch index_select / slice assignment with the kernels'
-semantics), each rank evaluates the RHS of its owned elements with the CPU
-oracle on its sub-mesh, and the distributed LSRK4 run must equal the
-single-process oracle run.
+The GPU path (DistributedMaxwellOperator) packs the face traces of the cut
+faces (dgm_trace_pack: 6 x Nfp values per (element, face) pair), exchanges
+them with NCCL send/recv and scatters them into the face nodes of the ghost
+rows (dgm_trace_unpack).  Here the same trace lists drive a CPU exchange over
+gloo (numpy gathers / scatters with the kernels' semantics; ghost nodes off
+the cut faces stay zero), each rank evaluates the RHS of its owned elements
+with the CPU oracle on its sub-mesh, and the distributed LSRK4 run must equal
+the single-process oracle run.
 """
 
 import os
@@ -72,6 +73,25 @@ def test_box_domains_reproduce_global_maps(world, order):
             k_own = doms[q].num_owned
             want = doms[q].ghost_global[begin - k_own:begin - k_own + cnt]
             assert np.array_equal(ids.astype(np.int64) + dr.owned[0], want)
+    # face traces: r's send list to q and q's receive list from r name the same (global element,
+    # face) pairs in the same order; each is a cut face (the neighbour across it is on the other rank)
+    for r, dr in enumerate(doms):
+        assert set(dr.send_traces) == set(dr.send) and set(dr.recv_traces) == set(dr.recv)
+        for q, tr in dr.send_traces.items():
+            sent = np.stack([tr[:, 0].astype(np.int64) + dr.owned[0], tr[:, 1]], 1)
+            rt = doms[q].recv_traces[r]
+            got = np.stack([doms[q].ghost_global[rt[:, 0] - doms[q].num_owned], rt[:, 1]], 1)
+            assert np.array_equal(sent, got)
+            across = gmaps.neighbors[sent[:, 0], sent[:, 1]]
+            q0, q1 = doms[q].owned
+            assert ((across >= q0) & (across < q1)).all() and (gmaps.codes[sent[:, 0], sent[:, 1]] >= 0).all()
+            # every (owned element, face) of r glued to q's range is listed exactly once
+            g0, g1 = dr.owned
+            nb, cd = gmaps.neighbors[g0:g1], gmaps.codes[g0:g1]
+            assert len(tr) == int(((cd >= 0) & (nb >= q0) & (nb < q1)).sum())
+        mdom = build_mesh_domain(mesh, elem, r, world, gmaps)
+        for q, tr in dr.send_traces.items():
+            assert np.array_equal(mdom.send_traces[q], tr) and np.array_equal(mdom.recv_traces[q], dr.recv_traces[q])
 
 
 def test_split_range_balanced():
@@ -86,21 +106,25 @@ def _free_port():
 
 
 def _exchange(dom, ext: torch.Tensor):
-    """Fill ext's ghost rows from their owners (CPU/gloo stand-in for dgm_halo_pack/unpack + NCCL)."""
+    """Fill the cut-face nodes of ext's ghost rows from their owners (CPU/gloo stand-in for
+    dgm_trace_pack / dgm_trace_unpack + NCCL): buffer[c][field][i] = u[field][elem][fmask[face][i]]."""
+    fmask = np.asarray(dom.elem.face_nodes)
+    x = ext.numpy()
     reqs, bufs = [], {}
-    for peer, ids in dom.send.items():
-        buf = ext.index_select(1, torch.as_tensor(ids, dtype=torch.long)).transpose(0, 1).contiguous()
+    for peer, tr in dom.send_traces.items():
+        e, f = tr[:, 0].astype(np.int64), tr[:, 1].astype(np.int64)
+        buf = torch.from_numpy(np.ascontiguousarray(x[:, e[:, None], fmask[f]].transpose(1, 0, 2)))
         reqs.append(dist.isend(buf, peer))
         bufs[("s", peer)] = buf
-    for peer, (begin, cnt) in dom.recv.items():
-        buf = torch.empty((cnt, 6, ext.shape[2]), dtype=ext.dtype)
+    for peer, tr in dom.recv_traces.items():
+        buf = torch.empty((len(tr), 6, fmask.shape[1]), dtype=ext.dtype)
         reqs.append(dist.irecv(buf, peer))
-        bufs[("r", peer)] = (buf, begin, cnt)
+        bufs[("r", peer)] = buf
     for r in reqs:
         r.wait()
-    for peer in dom.recv:
-        buf, begin, cnt = bufs[("r", peer)]
-        ext[:, begin:begin + cnt] = buf.transpose(0, 1)
+    for peer, tr in dom.recv_traces.items():
+        e, f = tr[:, 0].astype(np.int64), tr[:, 1].astype(np.int64)
+        x[:, e[:, None], fmask[f]] = bufs[("r", peer)].numpy().transpose(1, 0, 2)
 
 
 def _worker(rank, world, port, order, steps, dt, out_q):

@@ -283,3 +283,30 @@ def test_face_slot_order_and_code_tables(order):
         got = pm.code_table[pm.codes[inner, f]]                  # slot i -> neighbour node
         want = maps.code_table[maps.codes[inner, f]][:, perm[f]]  # natural node perm[f, i]
         assert np.array_equal(got, want)
+
+
+def test_tetgen_roundtrip_and_errors():
+    """read_tetgen: 0/1-based numbering, shuffled record order, bytes, comments, malformed input."""
+    from paper_0901_1024_b200 import MeshFormatError
+
+    mesh = generate_box_mesh((1.0, 2.0, 1.0), (2, 1, 2))
+    rng = np.random.default_rng(1)
+    for base in (0, 1):
+        # the numbering base is read from the first point record (reference behaviour), so it stays first
+        pord = np.concatenate([[0], 1 + rng.permutation(len(mesh.vertices) - 1)])
+        eord = rng.permutation(mesh.num_elements)
+        node = f"# comment\n{len(mesh.vertices)} 3 0 0\n" + "".join(
+            f"{i + base} {float(x)!r} {float(y)!r} {float(z)!r}  # pt\n" for i, (x, y, z) in zip(pord, mesh.vertices[pord]))
+        ele = f"{mesh.num_elements} 4 0\n" + "".join(
+            f"{i + base} " + " ".join(str(v + base) for v in mesh.elements[i]) + "\n" for i in eord)
+        got = read_tetgen(node.encode(), ele)
+        assert np.array_equal(got.vertices, mesh.vertices) and np.array_equal(got.elements, mesh.elements)
+    bad = [("4 3\n1 0 0 0\n2 1 0 0\n3 0 1 0\n", "1 4\n1 1 2 3 4\n"),          # fewer points than announced
+           ("4 3\n1 0 0 0\n1 1 0 0\n3 0 1 0\n4 0 0 1\n", "1 4\n1 1 2 3 4\n"),  # duplicate point id
+           ("4 3\n2 0 0 0\n3 1 0 0\n4 0 1 0\n5 0 0 1\n", "1 4\n2 2 3 4 5\n"),  # numbering starts at 2
+           ("4 3\n1 0 0 0\n2 1 0 0\n3 0 1 0\n4 0 0 z\n", "1 4\n1 1 2 3 4\n"),  # non-numeric coordinate
+           ("4 3\n1 0 0 0\n2 1 0 0\n3 0 1 0\n4 0 0 1\n", "1 4\n1 1 2 3\n"),    # short element record
+           ("4 3\n1 0 0 0\n2 1 0 0\n3 0 1 0\n4 0 0 1\n", "")]                  # empty .ele
+    for node, ele in bad:
+        with pytest.raises(MeshFormatError):
+            read_tetgen(node, ele)

@@ -355,7 +355,7 @@ def roofline(order, word, path, k, launch_s, peaks, pipes, kernel, traffic):
     b = bytes_per_element_stage(order, word) * k
     f = flops_per_element_stage(order) * k
     bw = peaks["hbm_gbs"] * 1e9
-    if path == "tensor" and pipes.get("tf32"):
+    if path in ("tensor", "tensor2") and pipes.get("tf32"):
         p, pipe = pipes["tf32"]["tflops"] * 1e12 / 3.0, "tensor"
         psrc = "3xTF32: measured kind::tf32 rate / 3 (" + pipes["tf32"]["source"] + ")"
     elif word == 8:
@@ -378,6 +378,8 @@ def roofline(order, word, path, k, launch_s, peaks, pipes, kernel, traffic):
 
 
 def _kernel_name(order, word, path):
+    if path == "tensor2":
+        return f"dgm::tc2_stage_kernel<{order},1>"
     if path == "tensor":
         return f"dgm::tc_stage_kernel<{order},1>"
     return f"dgm::stage_kernel<{order},{'float' if word == 4 else 'double'},1>"
@@ -385,7 +387,8 @@ def _kernel_name(order, word, path):
 
 def _traffic(ncu: dict, order: int, word: int, path: str):
     """ncu DRAM bytes per launch of this (kernel, order, dtype), or None if not captured."""
-    key = f"{'tc_stage_kernel' if path == 'tensor' else 'stage_kernel'}<{order}>/{'f32' if word == 4 else 'f64'}"
+    fam = {"tensor": "tc_stage_kernel", "tensor2": "tc2_stage_kernel"}.get(path, "stage_kernel")
+    key = f"{fam}<{order}>/{'f32' if word == 4 else 'f64'}"
     ent = ncu.get("kernels", {}).get(key)
     return {"bytes_per_launch": ent["dram_bytes_per_launch"], "key": key, "source": ent.get("source")} if ent else None
 
@@ -718,8 +721,8 @@ def main(argv=None) -> None:
                     help="natural host-state dtype of the e2e leg (default: float64, the reference's)")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--path", choices=("auto", "tensor", "simt"), default="auto",
-                    help="stage kernel: tcgen05 3xTF32 (tensor, fp32) or CUDA cores (simt)")
+    ap.add_argument("--path", choices=("auto", "tensor2", "tensor", "simt"), default="auto",
+                    help="stage kernel: tcgen05 3xTF32 v2 (tensor2, N<=4 fp32) or v1 (tensor), or CUDA cores (simt)")
     args = ap.parse_args(argv)
     if args.cells is None:
         args.cells = [110, 110, 110] if args.scaling == "strong" else list(CELLS)

@@ -72,9 +72,12 @@ typedef struct {
   int32_t tc_kv;            /* K offset of the first face block (3*npk up to 8) */
   int32_t tc_nfpk;          /* K extent of one face block (Nfp up to 8)       */
   int64_t tc_operand_floats;/* size of dgm_desc.tc_operand in floats          */
+  /* v2 tensor-core stage path (N <= 4, f32): state rows are the volume GEMM's A operand */
+  int32_t tc2_supported;
+  int64_t tc2_operand_floats;/* size of dgm_desc.tc2_operand in floats         */
 } dgm_layout_info;
 
-enum { DGM_PATH_AUTO = 0, DGM_PATH_SIMT = 1, DGM_PATH_TENSOR = 2 };
+enum { DGM_PATH_AUTO = 0, DGM_PATH_SIMT = 1, DGM_PATH_TENSOR = 2, DGM_PATH_TENSOR2 = 3 };
 
 /*
  * Operator description (replaces build_reference_operator, oracle.py:97-141).
@@ -108,7 +111,16 @@ enum { DGM_PATH_AUTO = 0, DGM_PATH_SIMT = 1, DGM_PATH_TENSOR = 2 };
  *                tf32 hi part and the exact fp32 remainder:
  *                tc_operand[s][h][c][n][q] = part_h(B[n][8s + 4c + q]).
  *                NULL disables the tensor-core path.
- *  path        : DGM_PATH_AUTO (tensor cores for fp32, N >= 2), _SIMT or _TENSOR.
+ *  tc2_operand : float[2*kv/4*nv*4 + 2*kf/4*nl*4], the v2 kernel's constant
+ *                operands (N <= 4; dgm_tc2.cuh): D = [hi | lo][kv/4][nv][4] with
+ *                row n = mu*mus + i holding D_mu[i][:] (mus = Np up to 4,
+ *                nv = 3 mus up to 16, kv = Np up to 8), then
+ *                LIFT = [hi | lo][kf/4][nl][4] with row i holding LIFT[i][f*Nfp+s]
+ *                at k = f*nfpk + s (nl = Np up to 16, nfpk = Nfp up to 8,
+ *                kf = 4 nfpk); zero elsewhere, hi = tf32 part, lo = exact remainder.
+ *                NULL disables the v2 path.
+ *  path        : DGM_PATH_AUTO (fp32: v2 tensor kernel when tc2_operand is given,
+ *                else tensor cores for N >= 2), _SIMT, _TENSOR (v1) or _TENSOR2.
  */
 typedef struct {
   int32_t order;
@@ -127,6 +139,7 @@ typedef struct {
   double permeability;
   const void* tc_operand;
   int32_t path;
+  const void* tc2_operand;
 } dgm_desc;
 
 typedef struct dgm_plan dgm_plan;
@@ -144,7 +157,7 @@ int dgm_layout(int32_t order, int32_t dtype, dgm_layout_info* out);
 int dgm_plan_create(const dgm_desc* desc, dgm_plan** out);
 int dgm_plan_destroy(dgm_plan* plan);
 
-/* Path the stage kernels of a plan run on: DGM_PATH_SIMT or DGM_PATH_TENSOR. */
+/* Path the stage kernels of a plan run on: DGM_PATH_SIMT, _TENSOR or _TENSOR2. */
 int dgm_plan_path(const dgm_plan* plan);
 
 /*

@@ -13,12 +13,12 @@ from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DGM_LIB") or os.path.join(_HERE, "libdgm.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 GEO_WORDS = 28
 
 DGM_F32, DGM_F64 = 0, 1
-PATH_AUTO, PATH_SIMT, PATH_TENSOR = 0, 1, 2
-PATHS = {"auto": PATH_AUTO, "simt": PATH_SIMT, "tensor": PATH_TENSOR}
+PATH_AUTO, PATH_SIMT, PATH_TENSOR, PATH_TENSOR2 = 0, 1, 2, 3
+PATHS = {"auto": PATH_AUTO, "simt": PATH_SIMT, "tensor": PATH_TENSOR, "tensor2": PATH_TENSOR2}
 _ERR_NAMES = {-1: "invalid argument", -2: "CUDA error", -3: "unsupported"}
 
 
@@ -34,7 +34,8 @@ class LayoutInfo(ctypes.Structure):
                 ("tile_elements", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("smem_bytes_fixed", ctypes.c_int64), ("tc_supported", ctypes.c_int32),
                 ("tc_nb", ctypes.c_int32), ("tc_steps", ctypes.c_int32), ("tc_npk", ctypes.c_int32),
-                ("tc_kv", ctypes.c_int32), ("tc_nfpk", ctypes.c_int32), ("tc_operand_floats", ctypes.c_int64)]
+                ("tc_kv", ctypes.c_int32), ("tc_nfpk", ctypes.c_int32), ("tc_operand_floats", ctypes.c_int64),
+                ("tc2_supported", ctypes.c_int32), ("tc2_operand_floats", ctypes.c_int64)]
 
 
 class Desc(ctypes.Structure):
@@ -45,7 +46,7 @@ class Desc(ctypes.Structure):
                 ("codes", ctypes.c_void_p), ("face_nodes", ctypes.c_void_p),
                 ("code_table", ctypes.c_void_p), ("num_codes", ctypes.c_int32),
                 ("permittivity", ctypes.c_double), ("permeability", ctypes.c_double),
-                ("tc_operand", ctypes.c_void_p), ("path", ctypes.c_int32)]
+                ("tc_operand", ctypes.c_void_p), ("path", ctypes.c_int32), ("tc2_operand", ctypes.c_void_p)]
 
 
 _I64, _VP, _D = ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
@@ -121,6 +122,8 @@ class Layout:
     tc_kv: int
     tc_nfpk: int
     tc_operand_floats: int
+    tc2_supported: int
+    tc2_operand_floats: int
 
 
 def layout(order: int, dtype: int) -> Layout:

@@ -15,8 +15,9 @@
 #include "dgm_aux.cuh"
 #include "dgm_stage.cuh"
 #include "dgm_tc.cuh"
+#include "dgm_tc2.cuh"
 
-#define DGM_ABI_VERSION 3
+#define DGM_ABI_VERSION 4
 
 namespace {
 
@@ -112,6 +113,7 @@ struct dgm_plan {
   size_t stage_smem;  // dynamic smem of the SIMT stage kernels
   int path;           // DGM_PATH_SIMT or DGM_PATH_TENSOR
   size_t tc_smem;     // dynamic smem of the tensor-core stage kernels
+  size_t tc2_smem;    // dynamic smem of the v2 tensor-core stage kernels (N <= 4)
   int num_sms;
   int device;         // CUDA device the plan was created on (DeviceGuard)
 };
@@ -142,6 +144,12 @@ DGM_TC_INFO(7)
 DGM_TC_INFO(8)
 DGM_TC_INFO(9)
 #undef DGM_TC_INFO
+
+template <int N>
+struct Tc2Info {
+  static constexpr bool supported = N <= 4;
+  static constexpr int64_t floats = supported ? (int64_t)dgm::Tc2Cfg<(N <= 4 ? N : 4)>::B_FLOATS : 0;
+};
 }  // namespace
 
 extern "C" {
@@ -173,6 +181,10 @@ int dgm_layout(int32_t order, int32_t dtype, dgm_layout_info* out) {
     out->tc_kv = TI::kv;
     out->tc_nfpk = TI::nfpk;
     out->tc_operand_floats = TI::floats;
+    using T2 = Tc2Info<decltype(n)::value>;
+    const bool f32 = sizeof(decltype(t)) == 4;
+    out->tc2_supported = (f32 && T2::supported) ? 1 : 0;
+    out->tc2_operand_floats = (f32 && T2::supported) ? T2::floats : 0;
     return DGM_OK;
   });
 }
@@ -219,14 +231,14 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
     return DGM_OK;
   });
   if (rc) return rc;
-  if (d.path < DGM_PATH_AUTO || d.path > DGM_PATH_TENSOR) return fail(DGM_ERR_INVALID, "bad path %d", d.path);
+  if (d.path < DGM_PATH_AUTO || d.path > DGM_PATH_TENSOR2) return fail(DGM_ERR_INVALID, "bad path %d", d.path);
   int path = DGM_PATH_SIMT;
   size_t tc_smem = 0;
   rc = dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
     constexpr int N = decltype(n)::value;
     using T = decltype(t);
     if constexpr (TcInfo<N, T>::supported) {
-      if (d.path == DGM_PATH_SIMT) return DGM_OK;
+      if (d.path == DGM_PATH_SIMT || d.path == DGM_PATH_TENSOR2) return DGM_OK;
       // AUTO: at N=1 the GEMM is too thin for the tensor cores to pay off (C2 sweep)
       if (d.path == DGM_PATH_AUTO && N < 2) return DGM_OK;
       if (!d.tc_operand || !aligned16(d.tc_operand)) {
@@ -258,6 +270,41 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
     }
   });
   if (rc) return rc;
+  // v2 tensor-core kernel (N <= 4, fp32): requested explicitly (DGM_PATH_TENSOR2) or by AUTO when the
+  // caller supplied its operand
+  size_t tc2_smem = 0;
+  if (d.path == DGM_PATH_TENSOR2 || (d.path == DGM_PATH_AUTO && d.tc2_operand)) {
+    rc = dispatch(d.order, d.dtype, [&](auto n, auto t) -> int {
+      constexpr int N = decltype(n)::value;
+      using T = decltype(t);
+      if constexpr (Tc2Info<N>::supported && sizeof(T) == 4) {
+        if (!d.tc2_operand || !aligned16(d.tc2_operand)) {
+          if (d.path == DGM_PATH_TENSOR2)
+            return fail(DGM_ERR_INVALID, "tensor2 path requested without a 16-byte aligned tc2_operand");
+          return DGM_OK;
+        }
+        using T2 = dgm::Tc2Cfg<N>;
+        tc2_smem = (T2::SMEM_FIXED + (size_t)d.num_codes * T2::NFP + 127) & ~size_t(127);
+        if (tc2_smem > 227 * 1024) {
+          if (d.path == DGM_PATH_TENSOR2) return fail(DGM_ERR_UNSUPPORTED, "tensor2 smem %zu too large", tc2_smem);
+          tc2_smem = 0;
+          return DGM_OK;
+        }
+        int r;
+        if ((r = raise_smem_limit(dgm::tc2_stage_kernel<N, dgm::MODE_RHS>, tc2_smem, "cudaFuncSetAttribute(tc2)")))
+          return r;
+        if ((r = raise_smem_limit(dgm::tc2_stage_kernel<N, dgm::MODE_LSRK>, tc2_smem, "cudaFuncSetAttribute(tc2)")))
+          return r;
+        path = DGM_PATH_TENSOR2;
+        return DGM_OK;
+      } else {
+        if (d.path == DGM_PATH_TENSOR2)
+          return fail(DGM_ERR_UNSUPPORTED, "no tensor2 path for order %d dtype %d", d.order, d.dtype);
+        return DGM_OK;
+      }
+    });
+    if (rc) return rc;
+  }
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   dgm_plan* p = new (std::nothrow) dgm_plan;
@@ -266,6 +313,7 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
   p->stage_smem = smem;
   p->path = path;
   p->tc_smem = tc_smem;
+  p->tc2_smem = tc2_smem;
   p->num_sms = sms > 0 ? sms : 148;
   p->device = dev;
   *out = p;
@@ -335,6 +383,28 @@ int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, vo
     args.yp = (T)(1.0 / z);
     args.inv_2z = (T)(1.0 / (2.0 * z));
     args.inv_2y = (T)(1.0 / (2.0 * (1.0 / z)));
+    if constexpr (Tc2Info<N>::supported && sizeof(T) == 4 && (MODE == dgm::MODE_RHS || MODE == dgm::MODE_LSRK)) {
+      if (plan->path == DGM_PATH_TENSOR2) {
+        using T2 = dgm::Tc2Cfg<N>;
+        dgm::Tc2Args targs;
+        targs.s = args;
+        targs.bops = static_cast<const float*>(d.tc2_operand);
+        const int64_t tt = (e_end - e_begin + T2::TE - 1) / T2::TE;
+        targs.num_tiles = (int)tt;
+        // persistent: one CTA per SM walks tiles blockIdx.x, + gridDim.x, ...
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(tt < plan->num_sms ? tt : plan->num_sms));
+        cfg.blockDim = dim3(T2::THREADS);
+        cfg.dynamicSmemBytes = plan->tc2_smem;
+        cfg.stream = static_cast<cudaStream_t>(stream);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cuda_check(cudaLaunchKernelEx(&cfg, dgm::tc2_stage_kernel<N, MODE>, targs), "tc2_stage_kernel launch");
+      }
+    }
     if constexpr (TcInfo<N, T>::supported && (MODE == dgm::MODE_RHS || MODE == dgm::MODE_LSRK)) {
       if (plan->path == DGM_PATH_TENSOR) {
         using TC = dgm::TcCfg<N>;

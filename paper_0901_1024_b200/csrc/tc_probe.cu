@@ -450,7 +450,7 @@ extern "C" int dgm_probe_mma_rate(int n, int reps, int ts, int nacc, long long* 
 
 extern "C" int dgm_probe_tf32_gemm_ts(const float* a, const float* b, float* c, int n, int k, int passes,
                                       void* stream) {
-  if (n < 16 || n > 256 || n % 16 || k < 8 || k > 64 || k % 8 || (passes != 1 && passes != 3)) return -1;
+  if (n < 16 || n > 256 || n % 16 || k < 8 || k > 64 || k % 8 || (passes != 1 && passes != 3 && passes != 13)) return -1;
   const size_t smem = (size_t)2 * n * k * sizeof(float);
   if (cudaFuncSetAttribute(probe_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return -2;
@@ -460,7 +460,7 @@ extern "C" int dgm_probe_tf32_gemm_ts(const float* a, const float* b, float* c, 
 
 extern "C" int dgm_probe_tf32_gemm(const float* a, const float* b, float* c, int n, int k, int passes,
                                    void* stream) {
-  if (n < 8 || n > 256 || n % 8 || k < 8 || k > 64 || k % 8 || (passes != 1 && passes != 3)) return -1;
+  if (n < 8 || n > 256 || n % 8 || k < 8 || k > 64 || k % 8 || (passes != 1 && passes != 3 && passes != 13)) return -1;
   const size_t smem = (size_t)2 * (128 + n) * k * sizeof(float);
   if (cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return -2;

@@ -69,13 +69,51 @@ def tc_operand(elem: ReferenceElement, lay, lift: np.ndarray | None = None) -> n
     return out
 
 
+def tc2_operand(elem: ReferenceElement, lift: np.ndarray | None = None) -> np.ndarray:
+    """Constant operands of the v2 tensor kernel, layout of dgm_desc.tc2_operand (include/dgm.h).
+
+    D part: B[n][j] = D_mu[i][j] for n = mu * mus + i (mus = Np up to 4), K = j up to kv = Np up to 8,
+    N = nv = 3 mus up to 16.  LIFT part: L[i][f * nfpk + s] = LIFT[i][f * Nfp + s], N = nl = Np up to 16.
+    Each as [hi | lo][K / 4 chunks][N rows][4]: hi = the tf32 part (13 low mantissa bits cleared),
+    lo = the remainder of the float64 operand in float32.
+    """
+    lift = elem.lift if lift is None else lift
+    n_p, n_fp = elem.num_nodes, elem.num_face_nodes
+    mus = (n_p + 3) // 4 * 4
+    nv, nl = (3 * mus + 15) // 16 * 16, (n_p + 15) // 16 * 16
+    kv, nfpk = (n_p + 7) // 8 * 8, (n_fp + 7) // 8 * 8
+    kf = 4 * nfpk
+    dmat = np.zeros((nv, kv))
+    for mu in range(3):
+        dmat[mu * mus:mu * mus + n_p, :n_p] = elem.diff[mu]
+    lmat = np.zeros((nl, kf))
+    for f in range(NUM_FACES):
+        lmat[:n_p, f * nfpk:f * nfpk + n_fp] = lift[:, f * n_fp:(f + 1) * n_fp]
+
+    def split_pack(mat):
+        hi = (mat.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+        lo = (mat - hi.astype(np.float64)).astype(np.float32)
+        rows, k = mat.shape
+        return [np.ascontiguousarray(x.reshape(rows, k // 4, 4).transpose(1, 0, 2)) for x in (hi, lo)]
+
+    parts = split_pack(dmat) + split_pack(lmat)
+    return np.concatenate([x.reshape(-1) for x in parts]).astype(np.float32)
+
+
 _SLOT_ORDERS: dict = {}
+# path="auto" picks the v2 tensor kernel for N <= 4 fp32 (set from measurements, DESIGN.md 3.2b)
+TC2_AUTO = False
 
 
-def _face_slot_order(elem: ReferenceElement) -> np.ndarray:
-    """ordering.face_slot_order for this element and layout, cached per order."""
-    from .ordering import face_slot_order
+def _face_slot_order(elem: ReferenceElement, v2: bool = False) -> np.ndarray:
+    """ordering.face_slot_order (v1 kernel) or face_slot_order_v2 for this element, cached per order."""
+    from .ordering import face_slot_order, face_slot_order_v2
 
+    if v2:
+        key = ("v2", elem.order)
+        if key not in _SLOT_ORDERS:
+            _SLOT_ORDERS[key] = face_slot_order_v2(elem.face_nodes, (elem.num_face_nodes + 7) // 8 * 8)
+        return _SLOT_ORDERS[key]
     if elem.order not in _SLOT_ORDERS:  # modelled on the fp32 tensor kernel's strides (TcCfg<N>)
         # the shared-memory row stride the kernel really uses (TcCfg::NPG = the f32 np_stride, an odd
         # number of 16-byte chunks), not ceil4(Np): they differ at N = 5, 7, 8
@@ -154,6 +192,10 @@ class B200MaxwellOperator:
         # the code table and the LIFT columns are permuted together, surface_flux maps back
         if path not in _capi.PATHS:
             raise ValueError(f"path must be one of {sorted(_capi.PATHS)}, got {path!r}")
+        # v2 tensor kernel (N <= 4, fp32): explicit, or the default where it is the faster kernel
+        self._use_tc2 = bool(lay.tc2_supported) and (path == "tensor2" or (path == "auto" and TC2_AUTO))
+        if path == "tensor2" and not lay.tc2_supported:
+            raise ValueError(f"no tensor2 path for order {elem.order} and {dtype}")
         if face_slots is None:
             face_slots = bool(lay.tc_supported) and path != "simt"
         lift = elem.lift
@@ -162,7 +204,7 @@ class B200MaxwellOperator:
         if face_slots:
             from .ordering import permute_face_slots
 
-            perm = _face_slot_order(elem)
+            perm = _face_slot_order(elem, v2=self._use_tc2)
             maps = permute_face_slots(maps, perm)
             n_fp = elem.num_face_nodes
             cols = (np.arange(NUM_FACES)[:, None] * n_fp + perm).reshape(-1)
@@ -196,8 +238,12 @@ class B200MaxwellOperator:
         self._ptab = dev(table, torch.uint8)
         self._num_codes = int(len(maps.code_table))
         self._tc = None
-        if lay.tc_supported and path != "simt":
+        if lay.tc_supported and path not in ("simt", "tensor2"):
             self._tc = dev(tc_operand(elem, lay, lift), torch.float32)
+        self._tc2 = None
+        if self._use_tc2:
+            self._tc2 = dev(tc2_operand(elem, lift), torch.float32)
+            assert self._tc2.numel() == lay.tc2_operand_floats
 
         desc = _capi.Desc(
             order=elem.order, dtype=self._dt_code, num_elements=self.num_elements,
@@ -207,7 +253,8 @@ class B200MaxwellOperator:
             codes=self._code.data_ptr(), face_nodes=self._fmask.data_ptr(),
             code_table=self._ptab.data_ptr(), num_codes=self._num_codes,
             permittivity=float(material.permittivity), permeability=float(material.permeability),
-            tc_operand=self._tc.data_ptr() if self._tc is not None else None, path=_capi.PATHS[path])
+            tc_operand=self._tc.data_ptr() if self._tc is not None else None, path=_capi.PATHS[path],
+            tc2_operand=self._tc2.data_ptr() if self._tc2 is not None else None)
         lib = _capi.load()
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
@@ -241,9 +288,9 @@ class B200MaxwellOperator:
 
     @property
     def path(self) -> str:
-        """'tensor' (tcgen05 3xTF32 stage kernel) or 'simt' (CUDA-core stage kernel)."""
+        """'tensor2' / 'tensor' (tcgen05 3xTF32 stage kernel v2 / v1) or 'simt' (CUDA-core stage kernel)."""
         code = self._lib.dgm_plan_path(self._plan)
-        return {_capi.PATH_SIMT: "simt", _capi.PATH_TENSOR: "tensor"}[code]
+        return {_capi.PATH_SIMT: "simt", _capi.PATH_TENSOR: "tensor", _capi.PATH_TENSOR2: "tensor2"}[code]
 
     @property
     def dofs(self) -> int:

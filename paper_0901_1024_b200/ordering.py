@@ -145,6 +145,58 @@ def face_slot_order(face_nodes: np.ndarray, order: int, np_stride: int, nfpk: in
     return perms
 
 
+def _v2_cost(nodes: np.ndarray, nfpk: int) -> int:
+    """Shared-memory wavefronts of the v2 kernel's owned-trace loads for one face slot order.
+
+    dgm_tc2.cuh: lane (e, b) of a flux warp loads node nodes[4b + jj] of element e for jj = 0..3;
+    the state tile stores node j of row e at bank (4e + j mod 4) mod 32, so the 8 elements of a warp
+    cover all banks once per residue and the cost of load jj is the largest number of blocks b whose
+    node has the same residue.  Padding slots (>= Nfp) read slot 0's node.
+    """
+    nfp = len(nodes)
+    cost = 0
+    for jj in range(4):
+        res = [int(nodes[s] if s < nfp else nodes[0]) % 4 for s in range(jj, nfpk, 4)]
+        cost += max(res.count(r) for r in set(res))
+    return cost
+
+
+def face_slot_order_v2(face_nodes: np.ndarray, nfpk: int) -> np.ndarray:
+    """(4, Nfp) slot permutation for the v2 tensor kernel (the v1 model is face_slot_order).
+
+    Pairwise-swap descent on _v2_cost from the natural order, then seeded restarts until every
+    column of slots reads four distinct residues (N=4: 16 -> 4 wavefronts per 4 loads) or the
+    budget is spent; deterministic.
+    """
+    face_nodes = np.asarray(face_nodes, dtype=np.int64)
+    nf, nfp = face_nodes.shape
+    floor = 4 * max(1, -(-(nfpk // 4) // 4)) if nfpk >= 16 else 4
+    rng = np.random.default_rng(0)
+    perms = np.empty((nf, nfp), dtype=np.int64)
+    for f in range(nf):
+        best, best_cost = None, None
+        for attempt in range(64):
+            perm = np.arange(nfp) if attempt == 0 else rng.permutation(nfp)
+            cur = _v2_cost(face_nodes[f][perm], nfpk)
+            improved = True
+            while improved:
+                improved = False
+                for a in range(nfp):
+                    for b in range(a + 1, nfp):
+                        perm[[a, b]] = perm[[b, a]]
+                        c = _v2_cost(face_nodes[f][perm], nfpk)
+                        if c < cur:
+                            cur, improved = c, True
+                        else:
+                            perm[[a, b]] = perm[[b, a]]
+            if best_cost is None or cur < best_cost:
+                best, best_cost = perm.copy(), cur
+            if best_cost <= floor:
+                break
+        perms[f] = best
+    return perms
+
+
 def permute_face_slots(maps: FaceMaps, perm: np.ndarray) -> FaceMaps:
     """FaceMaps whose face node i of face f is the natural face node perm[f, i].
 

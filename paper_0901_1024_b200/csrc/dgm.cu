@@ -1,4 +1,5 @@
 // dgm.cu -- C ABI of libdgm.so (see include/dgm.h for the contract).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -334,6 +335,38 @@ int dgm_plan_path(const dgm_plan* plan) {
 
 namespace {
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link needed).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 4-D view (node, element, t, h) of a (6, kf, npg) fp32 state-layout array, element extent e_end,
+// box {4 nodes, 64 elements, 1, 2} (dgm_tc2.cuh)
+int encode_state_map(CUtensorMap* m, const void* base, int npg, int64_t kf, int64_t e_end) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(DGM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[4] = {(cuuint64_t)npg, (cuuint64_t)e_end, 3, 2};
+  const cuuint64_t strides[3] = {(cuuint64_t)npg * 4, (cuuint64_t)kf * npg * 4, (cuuint64_t)3 * kf * npg * 4};
+  const cuuint32_t box[4] = {4, 64, 1, 2};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DGM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DGM_OK;
+}
+
 template <int MODE>
 int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, void* out, double a,
                  double b, double dt, int64_t e_begin, int64_t e_end, void* stream) {
@@ -389,6 +422,15 @@ int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, vo
         dgm::Tc2Args targs;
         targs.s = args;
         targs.bops = static_cast<const float*>(d.tc2_operand);
+        int r;
+        if ((r = encode_state_map(&targs.tm_u, u, C::NPG, d.field_stride, e_end))) return r;
+        if (MODE == dgm::MODE_LSRK) {
+          if ((r = encode_state_map(&targs.tm_res, res, C::NPG, d.field_stride, e_end))) return r;
+          if ((r = encode_state_map(&targs.tm_out, u_out, C::NPG, d.field_stride, e_end))) return r;
+        } else {
+          targs.tm_res = targs.tm_u;
+          if ((r = encode_state_map(&targs.tm_out, out, C::NPG, d.field_stride, e_end))) return r;
+        }
         const int64_t tt = (e_end - e_begin + T2::TE - 1) / T2::TE;
         targs.num_tiles = (int)tt;
         // persistent: one CTA per SM walks tiles blockIdx.x, + gridDim.x, ...

@@ -148,15 +148,17 @@ def face_slot_order(face_nodes: np.ndarray, order: int, np_stride: int, nfpk: in
 def _v2_cost(nodes: np.ndarray, nfpk: int) -> int:
     """Shared-memory wavefronts of the v2 kernel's owned-trace loads for one face slot order.
 
-    dgm_tc2.cuh: lane (e, b) of a flux warp loads node nodes[4b + jj] of element e for jj = 0..3;
-    the state tile stores node j of row e at bank (4e + j mod 4) mod 32, so the 8 elements of a warp
-    cover all banks once per residue and the cost of load jj is the largest number of blocks b whose
-    node has the same residue.  Padding slots (>= Nfp) read slot 0's node.
+    dgm_tc2.cuh: at step jj lane (e, b) of a flux warp loads node nodes[4b + (jj + b) % 4] of element
+    e (the rotation keeps its flux stores conflict-free); the state tile stores node j of row e at
+    bank (4e + j mod 4) mod 32, so the 8 elements of a warp cover all banks once per residue and the
+    cost of load jj is the largest number of blocks b whose node has the same residue.  Padding
+    slots (>= Nfp) read slot 0's node.
     """
     nfp = len(nodes)
     cost = 0
     for jj in range(4):
-        res = [int(nodes[s] if s < nfp else nodes[0]) % 4 for s in range(jj, nfpk, 4)]
+        slots = [4 * b + (jj + b) % 4 for b in range(nfpk // 4)]
+        res = [int(nodes[s] if s < nfp else nodes[0]) % 4 for s in slots]
         cost += max(res.count(r) for r in set(res))
     return cost
 

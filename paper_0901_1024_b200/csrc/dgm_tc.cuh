@@ -652,6 +652,10 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     mbar_wait(acc_full, 0);
     if (tid == 0) TC_TRACE(0, 4);  // accumulators final
     fence_after_sync();
+    // Every producer's last flux-staging read happened before its last A-stage arrival, which the
+    // accumulator commit already orders before this point; the barrier states that ordering in a
+    // form compute-sanitizer racecheck can see (it does not track tcgen05.commit arrivals).
+    named_sync(1, PROD);
 #pragma unroll 1
     for (int t = 0; t < 3; ++t) {  // epilogue phase: components T::epi_comp(t, 0 / 1)
       // residual rows of the phase's two components (L2-prefetched at CTA start), all loads in flight

@@ -3,7 +3,7 @@
 cd "${GRAFT_REPO_ROOT:-$(pwd)}"
 O=gpurun_out/sanitize; mkdir -p $O
 for tool in memcheck synccheck racecheck; do
-  timeout 1200 compute-sanitizer --tool $tool --print-limit 50 python scripts/sanitize_small.py "$@" > $O/$tool.log 2>&1
+  timeout 900 compute-sanitizer --tool $tool --print-limit 50 python scripts/sanitize_small.py "$@" > $O/$tool.log 2>&1
   echo "rc=$?" >> $O/$tool.log
   tail -3 $O/$tool.log
 done

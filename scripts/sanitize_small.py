@@ -2,7 +2,8 @@
 
 One or two CTAs per launch so the sanitizers finish: the N=4 tensor kernel on 48 and 96 tets
 (1 and 2 tiles of 64, one partial), N=6 tensor (1-CTA/SM kernel), N=8 (32-element tiles), N=4 fp64
-and N=1 fp32 SIMT, each as RHS and one LSRK4 step, checked against the oracle.
+and N=1 fp32 SIMT, the v2 tensor kernel at N=4 and N=3 (2 tiles), each as RHS and one LSRK4 step,
+checked against the oracle.
 """
 import os
 import sys
@@ -16,15 +17,17 @@ from oracle import build_oracle_operator  # noqa: E402
 from paper_0901_1024_b200 import build_b200_operator, build_reference_element, generate_box_mesh  # noqa: E402
 
 torch.cuda.set_device(0)
-cases = [((2, 2, 2), 4, torch.float32), ((4, 2, 2), 4, torch.float32), ((2, 2, 1), 6, torch.float32),
-         ((2, 1, 1), 8, torch.float32), ((2, 2, 2), 4, torch.float64), ((2, 2, 2), 1, torch.float32)]
+cases = [((2, 2, 2), 4, torch.float32, "auto"), ((4, 2, 2), 4, torch.float32, "auto"),
+         ((2, 2, 1), 6, torch.float32, "auto"), ((2, 1, 1), 8, torch.float32, "auto"),
+         ((2, 2, 2), 4, torch.float64, "auto"), ((2, 2, 2), 1, torch.float32, "auto"),
+         ((2, 2, 2), 4, torch.float32, "tensor2"), ((4, 2, 3), 3, torch.float32, "tensor2")]
 only = sys.argv[1:]
-for i, (cells, order, dtype) in enumerate(cases):
+for i, (cells, order, dtype, path) in enumerate(cases):
     if only and str(i) not in only:
         continue
     mesh = generate_box_mesh((1.0, 1.0, 1.0), cells)
     elem = build_reference_element(order)
-    op = build_b200_operator(mesh, elem, dtype=dtype)
+    op = build_b200_operator(mesh, elem, dtype=dtype, path=path)
     u0 = np.random.default_rng(i).normal(size=(6, mesh.num_elements, elem.num_nodes))
     got = op.rhs(u0)
     want = build_oracle_operator(mesh, elem).rhs(u0)

@@ -349,6 +349,40 @@ def measure_tf32_tflops(dev, sm_mhz: float) -> dict | None:
             "source": "probe: tcgen05.mma kind::tf32 M=128 N=48 K=8 (A in TMEM) bursts, measured in this run"}
 
 
+def measure_fp64_tflops(dev) -> dict | None:
+    """FP64 throughput of this GPU, measured in this run: DMMA (mma.sync m8n8k4 f64, the tensor pipe the
+    fp64 stage kernel's volume and LIFT products run on for N <= 6) and DFMA (the CUDA cores)."""
+    import ctypes
+
+    import torch
+
+    try:
+        lib = ctypes.CDLL(os.path.join(ROOT, "paper_0901_1024_b200", "libdgm_probe.so"))
+    except OSError:
+        return None
+    lib.dgm_probe_fp64_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    sink = torch.zeros(1, dtype=torch.float64, device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    out = {}
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        for name, tensor, flop_iter in (("dmma", 1, 8 * 8 * 512), ("dfma", 0, 256 * 8 * 2)):
+            blocks, iters = 8 * sms, 4096
+            best = None
+            for _ in range(3):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                if lib.dgm_probe_fp64_rate(tensor, blocks, iters, sink.data_ptr(), stream.cuda_stream) != 0:
+                    return None
+                e.record(stream)
+                torch.cuda.synchronize(dev)
+                ms = s.elapsed_time(e)
+                best = ms if best is None else min(best, ms)
+            out[name + "_tflops"] = blocks * iters * flop_iter / (best / 1e3) / 1e12
+    out["source"] = "probe kernels (8 blocks/SM x 8 warps, 8 independent chains), measured in this run"
+    return out
+
+
 def roofline(order, word, path, k, launch_s, peaks, pipes, kernel, traffic):
     from paper_0901_1024_b200.perfmodel import bytes_per_element_stage, flops_per_element_stage
 
@@ -358,6 +392,12 @@ def roofline(order, word, path, k, launch_s, peaks, pipes, kernel, traffic):
     if path in ("tensor", "tensor2") and pipes.get("tf32"):
         p, pipe = pipes["tf32"]["tflops"] * 1e12 / 3.0, "tensor"
         psrc = "3xTF32: measured kind::tf32 rate / 3 (" + pipes["tf32"]["source"] + ")"
+    elif word == 8 and order <= 6 and pipes.get("fp64"):
+        # fp64 N <= 6: volume + LIFT on DMMA, the rest on the CUDA cores; the faster measured pipe bounds it
+        f = pipes["fp64"]
+        p = max(f["dmma_tflops"], f["dfma_tflops"]) * 1e12
+        pipe, psrc = "fp64", ("FP64 (DMMA volume/LIFT): max of the measured DMMA %.1f and DFMA %.1f TFLOP/s (%s)"
+                              % (f["dmma_tflops"], f["dfma_tflops"], f["source"]))
     elif word == 8:
         p, pipe, psrc = pipes["fp64_tflops"] * 1e12, "fp64", "FP64 SIMT: SMs x 64 x 2 x max SM clock"
     else:
@@ -550,7 +590,7 @@ def run_b200(args) -> None:
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     pipes = {"fp32_tflops": sms * 128 * 2 * sm_max * 1e6 / 1e12, "fp64_tflops": sms * 64 * 2 * sm_max * 1e6 / 1e12,
-             "tf32": measure_tf32_tflops(dev, sm_max)}
+             "tf32": measure_tf32_tflops(dev, sm_max), "fp64": measure_fp64_tflops(dev)}
     ncu = _ncu_summary()
 
     with ClockSampler(local) as clocks:
@@ -682,7 +722,7 @@ def run_b200(args) -> None:
         "clocks": clk,
         "energy_after": energy,
         "pipes": {"fp32_simt_tflops": pipes["fp32_tflops"], "fp64_simt_tflops": pipes["fp64_tflops"],
-                  "tf32_mma": pipes["tf32"]},
+                  "tf32_mma": pipes["tf32"], "fp64_measured": pipes["fp64"]},
     }
     if extras:
         line["configs"] = extras
@@ -694,7 +734,7 @@ def run_b200(args) -> None:
 def _np_stride(order: int, word: int) -> int:
     from paper_0901_1024_b200 import _capi
 
-    return _capi.layout(order, 2 if word == 8 else 1).np_stride
+    return _capi.layout(order, _capi.DGM_F64 if word == 8 else _capi.DGM_F32).np_stride
 
 
 def main(argv=None) -> None:

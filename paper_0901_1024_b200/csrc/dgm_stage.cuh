@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "tc05.cuh"
+
 namespace dgm {
 
 constexpr int GEO_WORDS = 28;  // 26 used + 2 pad: rows are 7 x 16 B, so any row range is TMA-aligned
@@ -59,15 +61,26 @@ struct Cfg {
   static constexpr int G = W == 8 ? DGM_SIMT_G64 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
   static constexpr int E = W == 8 ? DGM_SIMT_E64 : 4;
 #else
-  // element groups x elements per thread; fp64 N=3 and N=6 run one element per thread
-  // (229 vs 264 us and 1.66 vs 2.11 ms per stage at 48k tets; other orders are faster with two)
-  static constexpr bool E1 = W == 8 && (N == 3 || N == 6);
-  static constexpr int G = E1 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
-  static constexpr int E = E1 ? 1 : ((W == 4) ? 4 : 2);
+  // element groups x elements per thread (SIMT P2 and the mass norm); fp64 N <= 6 runs P2 on DMMA
+  // with tiles of 16 elements (two 8-column MMA tiles): N=6 as 4 groups x 4 elements
+  static constexpr bool F64N6 = W == 8 && N == 6;
+  static constexpr int G = F64N6 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
+  static constexpr int E = F64N6 ? 4 : ((W == 4) ? 4 : 2);
 #endif
   static constexpr int TE = G * E;                           // elements per tile
   static constexpr int WORK = NP * G;
-  static constexpr int THREADS = ((WORK + 31) / 32) * 32;
+  // fp64 volume + LIFT on the FP64 tensor path (mma.sync m8n8k4 f64, DMMA): one warp task = 8 nodes x
+  // 8 elements x one field half; N >= 7 keeps the SIMT P2 (tiles of <= 8 elements there)
+#ifdef DGM_F64_SIMT_P2
+  static constexpr bool DMMA = false;
+#else
+  static constexpr bool DMMA = W == 8 && N <= 6 && TE % 8 == 0;
+#endif
+  static constexpr int NIT = (NP + 7) / 8;                   // DMMA node tiles
+  static constexpr int DTASKS = NIT * (TE / 8) * 2;
+  static constexpr int DWARPS = DTASKS < 10 ? DTASKS : 10;
+  static constexpr int THREADS_SIMT = ((WORK + 31) / 32) * 32;
+  static constexpr int THREADS = (DMMA && 32 * DWARPS > THREADS_SIMT) ? 32 * DWARPS : THREADS_SIMT;
   static_assert(NF4 >= NP, "rhs rows reuse the flux buffer");
   static constexpr size_t SMEM_REAL = (size_t)6 * TE * NPG + (size_t)6 * TE * NFS + (size_t)TE * GEO_WORDS;
   static constexpr size_t SMEM_FIXED = SMEM_REAL * W + (size_t)TE * 8 * 4 + 4 * NFP;
@@ -145,6 +158,14 @@ __device__ __forceinline__ void upwind(const T* um, const T* up, T nx, T ny, T n
   for (int c = 3; c < 6; ++c) out[c] *= a.inv_2y;
 }
 
+// D(8x8) += A(8x4, row) B(4x8, col) in fp64 on the tensor pipe; lane l holds A[l/4][l%4],
+// B[l%4][l/4] and D[l/4][2(l%4) + {0, 1}].
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
 template <int N, typename T, int MODE>
 __global__ void __launch_bounds__(Cfg<N, T>::THREADS, Cfg<N, T>::MIN_BLOCKS)
 stage_kernel(const StageArgs<T> a) {
@@ -168,29 +189,42 @@ stage_kernel(const StageArgs<T> a) {
   const int64_t fstride = a.kf * NPG;
 
   // ---------------- P0: stage the tile ----------------
+  // one thread issues bulk copies of the tile's rows (6 field slabs, geometry, connectivity) on an
+  // mbarrier and warms L2 with the residual rows the write-back reads; the others zero the rows of
+  // a partial tile and copy the face tables meanwhile
+  __shared__ __align__(8) uint64_t s_bar;
   {
     constexpr int RV = NPG / VEC;  // 16-byte chunks per u row
-    const int nvec = nv * RV;
-    const V* src = reinterpret_cast<const V*>(a.u + e0 * NPG);
-    V* dst = reinterpret_cast<V*>(s_u);
-    const V zero = {};
-#pragma unroll 1
-    for (int f = 0; f < 6; ++f) {
-      const V* sf = src + (size_t)f * (fstride / VEC);
-      V* df = dst + f * TE * RV;
-      for (int c = tid; c < TE * RV; c += blockDim.x) df[c] = (c < nvec) ? sf[c] : zero;
+    if (tid == 0) {
+      tc::mbar_init(&s_bar, 1);
+      tc::mbar_init_fence();
     }
-    const T* gsrc = a.geo + e0 * GEO_WORDS;
-    for (int c = tid; c < TE * GEO_WORDS; c += blockDim.x)
-      s_geo[c] = (c < nv * GEO_WORDS) ? gsrc[c] : T(0);
-    if (MODE != MODE_VOLUME) {
-      for (int c = tid; c < nv * 4; c += blockDim.x) {
-        s_nbr[c] = a.nbr[e0 * 4 + c];
-        s_code[c] = a.code[e0 * 4 + c];
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t rowb = (uint32_t)nv * NPG * sizeof(T), geob = (uint32_t)nv * GEO_WORDS * sizeof(T);
+      const uint32_t conb = (uint32_t)nv * 16;
+      tc::mbar_expect_tx(&s_bar, 6 * rowb + geob + (MODE != MODE_VOLUME ? 2 * conb : 0));
+#pragma unroll 1
+      for (int f = 0; f < 6; ++f) tc::bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowb, &s_bar);
+      tc::bulk_g2s(s_geo, a.geo + e0 * GEO_WORDS, geob, &s_bar);
+      if (MODE != MODE_VOLUME) {
+        tc::bulk_g2s(s_nbr, a.nbr + e0 * 4, conb, &s_bar);
+        tc::bulk_g2s(s_code, a.code + e0 * 4, conb, &s_bar);
       }
+      if (MODE == MODE_LSRK && !a.a_zero)
+        for (int f = 0; f < 6; ++f) tc::prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rowb);
+    }
+    if (nv < TE) {
+      const V zero = {};
+      for (int f = 0; f < 6; ++f)
+        for (int c = nv * RV + tid; c < TE * RV; c += blockDim.x) reinterpret_cast<V*>(s_u + f * TE * NPG)[c] = zero;
+      for (int c = nv * GEO_WORDS + tid; c < TE * GEO_WORDS; c += blockDim.x) s_geo[c] = T(0);
+    }
+    if (MODE != MODE_VOLUME) {
       for (int c = tid; c < 4 * NFP; c += blockDim.x) s_fmask[c] = a.fmask[c];
       for (int c = tid; c < a.ncodes * NFP; c += blockDim.x) s_ptab[c] = a.ptab[c];
     }
+    tc::mbar_wait(&s_bar, 0);
   }
   __syncthreads();
 
@@ -252,6 +286,84 @@ stage_kernel(const StageArgs<T> a) {
     return;
   }
 
+  // ---------------- P2 (fp64, N <= 6): volume + lift on DMMA ----------------
+  if constexpr (C::DMMA) {
+    // task (node tile it, element half eh, field half hh): the 3 derivatives of fields 3hh..3hh+2
+    // (rows i, K = node j of D_mu; columns = the 8 elements) and the lifted flux of components
+    // 3(1-hh)..+2 (K = face node), i.e. the whole update of those components; the curl is formed
+    // from the accumulator fragments (lane: node 8 it + l/4, elements 8 eh + 2(l%4) + {0, 1})
+    constexpr int NEH = TE / 8, NT = C::NIT * NEH * 2, NWARPS = C::THREADS / 32;
+    constexpr int MAXT = (NT + NWARPS - 1) / NWARPS;
+    constexpr int KJ = (NP + 3) / 4 * 4, NF4 = C::NF4;
+    const int warp = tid >> 5, lane = tid & 31, g4 = lane >> 2, t4 = lane & 3;
+    T keep[MAXT][3][2];
+#pragma unroll
+    for (int q = 0; q < MAXT; ++q) {
+      const int task = warp + q * NWARPS;
+      if (task >= NT) break;
+      const int hh = task & 1, rest = task >> 1, eh = rest % NEH, it = rest / NEH;
+      const int i = 8 * it + g4;   // A row / accumulator row: node
+      const int eb = 8 * eh + g4;  // B column: element
+      T acc[3][3][2], accl[3][2];
+#pragma unroll
+      for (int mu = 0; mu < 3; ++mu)
+#pragma unroll
+        for (int t = 0; t < 3; ++t) acc[mu][t][0] = acc[mu][t][1] = T(0);
+#pragma unroll
+      for (int t = 0; t < 3; ++t) accl[t][0] = accl[t][1] = T(0);
+#pragma unroll 3
+      for (int k0 = 0; k0 < KJ; k0 += 4) {
+        const int k = k0 + t4;
+        T av[3], bv[3];
+#pragma unroll
+        for (int mu = 0; mu < 3; ++mu)
+          av[mu] = (i < NP && k < NP) ? __ldg(a.diff + (((size_t)mu * C::NJC + (k >> 1)) * NP + i) * 2 + (k & 1)) : T(0);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) bv[t] = s_u[((3 * hh + t) * TE + eb) * NPG + k];  // rows zero past Np
+#pragma unroll
+        for (int mu = 0; mu < 3; ++mu)
+#pragma unroll
+          for (int t = 0; t < 3; ++t) dmma_8x8x4(acc[mu][t], av[mu], bv[t]);
+      }
+      if (MODE != MODE_VOLUME) {
+#pragma unroll 3
+        for (int k0 = 0; k0 < NF4; k0 += 4) {
+          const int k = k0 + t4;
+          const T al = i < NP ? __ldg(a.lift + ((size_t)(k >> 1) * NP + i) * 2 + (k & 1)) : T(0);
+#pragma unroll
+          for (int t = 0; t < 3; ++t) dmma_8x8x4(accl[t], al, s_fl[((3 * (1 - hh) + t) * TE + eb) * NFS + k]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int e = 8 * eh + 2 * t4 + c;
+        const T* gk = s_geo + e * GEO_WORDS;
+        // grad_nu F_t = sum_mu rx[mu][nu] dF_t/dr_mu; (curl F)_t = grad_t1 F_t2 - grad_t2 F_t1
+        auto grad = [&](int nu, int t) {
+          return gk[nu] * acc[0][t][c] + gk[3 + nu] * acc[1][t][c] + gk[6 + nu] * acc[2][t][c];
+        };
+        const T curl[3] = {grad(1, 2) - grad(2, 1), grad(2, 0) - grad(0, 2), grad(0, 1) - grad(1, 0)};
+        const T sgn = hh ? T(1) : T(-1), mat = hh ? a.inv_eps : a.inv_mu;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) keep[q][t][c] = (sgn * curl[t] + accl[t][c] * gk[9]) * mat;
+      }
+    }
+    if (MODE != MODE_VOLUME) __syncthreads();  // every lift read of s_fl is done
+#pragma unroll
+    for (int q = 0; q < MAXT; ++q) {
+      const int task = warp + q * NWARPS;
+      if (task >= NT) break;
+      const int hh = task & 1, rest = task >> 1, eh = rest % NEH, it = rest / NEH;
+      const int i = 8 * it + g4;
+      if (i < NP) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int t = 0; t < 3; ++t) s_fl[((3 * (1 - hh) + t) * TE + 8 * eh + 2 * t4 + c) * NFS + i] = keep[q][t][c];
+      }
+    }
+    __syncthreads();
+  } else {
   // ---------------- P2: volume + lift ----------------
   T rhs[6][E];
   const bool worker = tid < C::WORK;
@@ -341,6 +453,7 @@ stage_kernel(const StageArgs<T> a) {
       for (int e = 0; e < E; ++e) s_fl[(f * TE + e * G + g) * NFS + i] = rhs[f][e];
   }
   __syncthreads();
+  }  // SIMT P2
 
   // ---------------- P3: coalesced write-back ----------------
   {

@@ -486,3 +486,49 @@ extern "C" int dgm_probe_mma_shape(int reps, int variant, int ctas, long long* c
   probe_shape_kernel<<<ctas, 128, 48 * 16 * 4 + 1024>>>(reps, variant, cycles_dev);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
+
+// FP64 tensor-pipe (DMMA, mma.sync m8n8k4 f64) throughput: every warp runs `iters` rounds of 8
+// independent MMAs; the caller times the launch.  flop = blocks * warps * iters * 8 * 512.
+__global__ void __launch_bounds__(256) probe_dmma_kernel(int iters, double* sink) {
+  double c[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = 0.0;
+  const double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * threadIdx.x;
+  for (int r = 0; r < iters; ++r) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[q][0]), "+d"(c[q][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += c[q][0] + c[q][1];
+  if (s == 12345.0) sink[0] = s;
+}
+
+// FP64 SIMT (DFMA) throughput: 8 independent chains per thread, `iters` rounds.
+// flop = blocks * 256 * iters * 8 * 2.
+__global__ void __launch_bounds__(256) probe_dfma_kernel(int iters, double* sink) {
+  double c[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c[q] = 1e-3 * q;
+  const double a = 1.0 + 1e-9 * threadIdx.x, b = 1e-12;
+  for (int r = 0; r < iters; ++r) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) c[q] = fma(c[q], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += c[q];
+  if (s == 12345.0) sink[0] = s;
+}
+
+extern "C" int dgm_probe_fp64_rate(int tensor, int blocks, int iters, double* sink, void* stream) {
+  if (blocks < 1 || iters < 1) return -1;
+  if (tensor)
+    probe_dmma_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(iters, sink);
+  else
+    probe_dfma_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(iters, sink);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}

@@ -532,3 +532,31 @@ extern "C" int dgm_probe_fp64_rate(int tensor, int blocks, int iters, double* si
     probe_dfma_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(iters, sink);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
+
+// Legacy warp-level TF32 MMA (mma.sync m16n8k8 tf32, fp32 accumulate) throughput: 8 independent
+// accumulators per warp, `iters` rounds; flop = blocks * 8 warps * iters * 8 * 2048.
+__global__ void __launch_bounds__(256) probe_tf32sync_kernel(int iters, float* sink) {
+  float c[8][4];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = c[q][2] = c[q][3] = 0.f;
+  const uint32_t a0 = __float_as_uint(1.0f + 1e-6f * threadIdx.x), a1 = a0, a2 = a0, a3 = a0;
+  const uint32_t b0 = __float_as_uint(0.5f), b1 = b0;
+  for (int r = 0; r < iters; ++r) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      asm volatile(
+          "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+          : "+f"(c[q][0]), "+f"(c[q][1]), "+f"(c[q][2]), "+f"(c[q][3])
+          : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += c[q][0] + c[q][1] + c[q][2] + c[q][3];
+  if (s == 12345.f) sink[0] = s;
+}
+
+extern "C" int dgm_probe_tf32sync_rate(int blocks, int iters, float* sink, void* stream) {
+  if (blocks < 1 || iters < 1) return -1;
+  probe_tf32sync_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(iters, sink);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}

@@ -394,10 +394,10 @@ def roofline(order, word, path, k, launch_s, peaks, pipes, kernel, traffic):
         psrc = "3xTF32: measured kind::tf32 rate / 3 (" + pipes["tf32"]["source"] + ")"
     elif word == 8 and order <= 6 and pipes.get("fp64"):
         # fp64 N <= 6: volume + LIFT on DMMA, the rest on the CUDA cores; the faster measured pipe bounds it
-        f = pipes["fp64"]
-        p = max(f["dmma_tflops"], f["dfma_tflops"]) * 1e12
+        f64 = pipes["fp64"]
+        p = max(f64["dmma_tflops"], f64["dfma_tflops"]) * 1e12
         pipe, psrc = "fp64", ("FP64 (DMMA volume/LIFT): max of the measured DMMA %.1f and DFMA %.1f TFLOP/s (%s)"
-                              % (f["dmma_tflops"], f["dfma_tflops"], f["source"]))
+                              % (f64["dmma_tflops"], f64["dfma_tflops"], f64["source"]))
     elif word == 8:
         p, pipe, psrc = pipes["fp64_tflops"] * 1e12, "fp64", "FP64 SIMT: SMs x 64 x 2 x max SM clock"
     else:
@@ -425,10 +425,10 @@ def _kernel_name(order, word, path):
     return f"dgm::stage_kernel<{order},{'float' if word == 4 else 'double'},1>"
 
 
-def _traffic(ncu: dict, order: int, word: int, path: str):
-    """ncu DRAM bytes per launch of this (kernel, order, dtype), or None if not captured."""
+def _traffic(ncu: dict, order: int, word: int, path: str, elements: int):
+    """ncu DRAM bytes per launch of this (kernel, order, dtype, mesh size), or None if not captured."""
     fam = {"tensor": "tc_stage_kernel", "tensor2": "tc2_stage_kernel"}.get(path, "stage_kernel")
-    key = f"{fam}<{order}>/{'f32' if word == 4 else 'f64'}"
+    key = f"{fam}<{order}>/{'f32' if word == 4 else 'f64'}@{elements}"
     ent = ncu.get("kernels", {}).get(key)
     return {"bytes_per_launch": ent["dram_bytes_per_launch"], "key": key, "source": ent.get("source")} if ent else None
 
@@ -494,7 +494,7 @@ def run_extra(name, spec, dev, clocks, peaks, pipes, ncu) -> dict:
            "value": flops_per_element_stage(order) * k * 5 * steps / sec / 1e9, "unit": UNIT,
            "dof_updates_per_s": dofs(order, k) * steps / sec, "setup_s": round(setup_s, 2),
            "roofline": roofline(order, word, op.path, k, launch_s, peaks, pipes, _kernel_name(order, word, op.path),
-                                _traffic(ncu, order, word, op.path)),
+                                _traffic(ncu, order, word, op.path, k)),
            "energy_after": energy}
     del op, u
     torch.cuda.empty_cache()
@@ -710,7 +710,7 @@ def run_b200(args) -> None:
                    "setup_s": round(setup_s, 2), "flops_per_element_stage": f_alg,
                    "bytes_per_element_stage": b_alg},
         "roofline": roofline(args.order, word, path, k, launch_s, peaks, pipes,
-                             _kernel_name(args.order, word, path), _traffic(ncu, args.order, word, path)),
+                             _kernel_name(args.order, word, path), _traffic(ncu, args.order, word, path, k)),
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_gflops, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,

@@ -107,7 +107,10 @@ struct TcCfg {
   static constexpr int MAP = SMALL ? 2 : (N <= 6 ? 0 : (N <= 8 ? 1 : 2));
   static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? 32 : 16);  // elements per CTA
   static constexpr int MT = MAP == 0 ? 3 : (MAP == 1 ? 2 : 1);     // M-tiles
-#ifdef DGM_TC_W16
+#if defined(DGM_TC_WIDE_MASK)
+  // experiment knob: bit N set -> 16 producer warps with 2 K-columns per thread at order N
+  static constexpr bool WIDE = ((DGM_TC_WIDE_MASK) >> N) & 1;
+#elif defined(DGM_TC_W16)
   static constexpr bool WIDE = N <= 4;   // experiment: 16 producer warps, 2 K-columns per thread
 #else
   static constexpr bool WIDE = false;

@@ -103,6 +103,8 @@ def tc2_operand(elem: ReferenceElement, lift: np.ndarray | None = None) -> np.nd
 _SLOT_ORDERS: dict = {}
 # path="auto" picks the v2 tensor kernel for N <= 4 fp32 (set from measurements)
 TC2_AUTO = False
+# path="auto" runs fp32 N <= 3 meshes with fewer elements than this on the CUDA-core kernel
+SMALL_MESH_SIMT = 64 * 148
 
 
 def _face_slot_order(elem: ReferenceElement, v2: bool = False) -> np.ndarray:
@@ -192,6 +194,10 @@ class B200MaxwellOperator:
         # the code table and the LIFT columns are permuted together, surface_flux maps back
         if path not in _capi.PATHS:
             raise ValueError(f"path must be one of {sorted(_capi.PATHS)}, got {path!r}")
+        if path == "auto" and dtype == torch.float32 and elem.order <= 3 and len(det_j) < SMALL_MESH_SIMT:
+            # a few tiles per GPU: the CUDA-core kernel's shorter per-tile latency wins (C1, 1,512 tets
+            # at N=3: 14.2 vs 17.9 us per stage, profiles/r02/paths.jsonl)
+            path = "simt"
         # v2 tensor kernel (N <= 4, fp32): explicit, or the default where it is the faster kernel
         self._use_tc2 = bool(lay.tc2_supported) and (path == "tensor2" or (path == "auto" and TC2_AUTO))
         if path == "tensor2" and not lay.tc2_supported:

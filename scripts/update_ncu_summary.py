@@ -2,8 +2,8 @@
 
     python scripts/update_ncu_summary.py KEY=path/to/summary.csv [KEY=...]
 
-KEY is "<kernel family><N>/<dtype>", e.g. tc2_stage_kernel<4>/f32 -- what bench.py's _traffic looks
-up.  Stored per launch: DRAM bytes read + written, duration, the kernel name and the source file.
+KEY is "<kernel family><N>/<dtype>@<elements>", e.g. tc_stage_kernel<4>/f32@998250 -- what bench.py's
+_traffic looks up (the mesh size is part of the key: traffic per launch scales with it).  Stored per launch: DRAM bytes read + written, duration, the kernel name and the source file.
 """
 import csv
 import json
@@ -36,7 +36,10 @@ def main(args):
     data.setdefault("kernels", {})
     for a in args:
         key, path = a.split("=", 1)
-        data["kernels"][key] = read(path)
+        ent = read(path)
+        if "@" in key:
+            ent["elements"] = int(key.split("@", 1)[1])
+        data["kernels"][key] = ent
     json.dump(data, open(OUT, "w"), indent=1)
 
 

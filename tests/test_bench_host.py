@@ -56,3 +56,20 @@ def test_measured_peaks_parsing(tmp_path, monkeypatch, data, want, key):
     (tmp_path / "MEASURED_PEAKS.json").write_text(json.dumps(data))
     got = bench._peaks()
     assert got["hbm_gbs"] == pytest.approx(want) and got["source"].endswith(key)
+
+
+@pytest.mark.parametrize("order,word,path,bound", [(4, 4, "tensor", "hbm"), (4, 8, "simt", "fp64"),
+                                                   (9, 4, "tensor", "tensor"), (7, 8, "simt", "fp64"),
+                                                   (1, 4, "simt", "hbm"), (4, 4, "tensor2", "hbm")])
+def test_roofline_model_names_the_binding_term(order, word, path, bound):
+    """T_roof = max(B_alg / BW, F_alg / P) with P the pipe the kernel computes on."""
+    peaks = {"hbm_gbs": 6548.8, "source": "test"}
+    pipes = {"fp32_tflops": 74.4, "fp64_tflops": 37.2,
+             "tf32": {"tflops": 1152.0, "source": "test"},
+             "fp64": {"dmma_tflops": 37.1, "dfma_tflops": 36.0, "source": "test"}}
+    r = bench.roofline(order, word, path, 998250, 1e-3, peaks, pipes, "k", None)
+    assert r["bound"] == bound
+    assert r["frac"] == pytest.approx(max(r["hbm_term_us"], r["compute_term_us"]) / 1e3)
+    assert r["unit"] == ("GB/s" if bound == "hbm" else "TFLOP/s")
+    pipes_no_probe = dict(pipes, tf32=None, fp64=None)
+    assert bench.roofline(order, word, path, 998250, 1e-3, peaks, pipes_no_probe, "k", None)["frac"] > 0

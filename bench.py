@@ -528,7 +528,7 @@ def run_b200(args) -> None:
         mesh = generate_box_mesh((1.0, 1.0, 1.0), cells)
         op = build_b200_operator(mesh, elem, dtype=dtype, device=dev, path=args.path,
                                  reorder={"auto": None, "natural": False, "morton": "morton",
-                                          "columns": True}[args.element_order],
+                                          "columns": True, "greedy": "greedy"}[args.element_order],
                                  face_slots=None if args.face_slots == "auto" else False)
         dt = stable_dt(mesh, op.geometry, args.order)
         extent = (1.0, 1.0, 1.0)
@@ -753,7 +753,7 @@ def main(argv=None) -> None:
                     help="extra config rows at N=1: default (%s), all, none, or a comma list of %s"
                          % (",".join(DEFAULT_EXTRAS), ",".join(EXTRAS)))
     ap.add_argument("--e2e-steps", type=int, default=None, help="e2e steps (default: --steps)")
-    ap.add_argument("--element-order", choices=("auto", "natural", "morton", "columns"), default="auto",
+    ap.add_argument("--element-order", choices=("auto", "natural", "morton", "columns", "greedy"), default="auto",
                     help="internal element numbering (ordering.py); auto = Morton where it pays")
     ap.add_argument("--face-slots", choices=("auto", "natural"), default="auto",
                     help="node order inside each face (ordering.face_slot_order); auto = bank-spread on the tensor path")

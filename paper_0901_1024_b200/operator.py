@@ -648,7 +648,8 @@ def build_b200_operator(mesh: Mesh, elem: ReferenceElement, material: Material =
     """Drop-in for build_reference_operator (oracle.py:97-141) on one B200.
 
     ``reorder=True`` numbers the elements internally in 2x2-cell columns of their centroids
-    (``"morton"``: along a Morton curve; paper_0901_1024_b200/ordering.py); the natural-order API
+    (``"morton"``: along a Morton curve; ``"greedy"``: the paper's Alg. 2 face-adjacency blocks of
+    64, reference layout.py:59-117; paper_0901_1024_b200/ordering.py); the natural-order API
     is unchanged.  Default (None): on for 2 <= N <= 8 (C3 fp32 1.63 -> 1.54 ms per stage, fp64
     and N = 7, 8 0.4-1.3 % faster; N = 1 and N = 9 keep the reference numbering).
     ``face_slots`` (default: whenever the tensor path is available) renumbers the nodes inside
@@ -664,8 +665,11 @@ def build_b200_operator(mesh: Mesh, elem: ReferenceElement, material: Material =
     if reorder:
         from . import ordering
 
-        fn = ordering.morton_order if reorder == "morton" else ordering.column_order
-        order = fn(mesh.vertices, mesh.elements)
+        if reorder == "greedy":  # the paper's Alg. 2 blocks (reference layout.py:59-117), tile-sized
+            order = ordering.greedy_block_order(mesh.vertices, mesh.elements, 64, connectivity)
+        else:
+            fn = ordering.morton_order if reorder == "morton" else ordering.column_order
+            order = fn(mesh.vertices, mesh.elements)
     op = B200MaxwellOperator(elem, material, geometry_words(geometry), geometry.det_jacobians, maps,
                              dtype=dtype, device=device, path=path, order=order, face_slots=face_slots)
     op.mesh = mesh

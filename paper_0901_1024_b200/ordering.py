@@ -222,3 +222,106 @@ def permute_face_slots(maps: FaceMaps, perm: np.ndarray) -> FaceMaps:
     code_table = np.array(table, dtype=np.uint8).reshape(len(table), perm.shape[1])
     return FaceMaps(num_nodes=maps.num_nodes, face_nodes=face_nodes, neighbors=maps.neighbors,
                     codes=new_codes, code_table=code_table)
+
+
+# ---------------------------------------------------------------------------
+# The paper's Alg. 2 partitioner (reference layout.py:59-117, greedy_partition), as an element order.
+
+
+def greedy_partition(mesh, max_block_size: int, connectivity=None) -> list:
+    """Connected blocks of at most ``max_block_size`` elements, identical to the reference's Alg. 2.
+
+    Breadth-first agglomeration: the growing block absorbs the queued candidate sharing the most faces
+    with it (ties: the earliest queued entry); a full block reseeds from the queue's front entry, an
+    exhausted queue from the lowest remaining element id.  The reference rescans its whole queue per
+    pick (quadratic in the block's frontier); here the queue is an append-only array with a heap keyed
+    (-shared faces, queue position) and lazy invalidation, so it runs in O(K log K) and reproduces the
+    reference's blocks exactly (tests/test_setup.py, golden partitions made by the reference itself).
+    """
+    import heapq
+
+    if max_block_size < 1:
+        raise ValueError("max_block_size must be >= 1")
+    if connectivity is None:
+        from .mesh import build_connectivity
+
+        connectivity = build_connectivity(mesh)
+    k = int(mesh.num_elements)
+    # neighbour lists in the reference's order: interior pairs in connectivity order, both directions
+    em = np.asarray(connectivity.elem_minus, dtype=np.int64)
+    ep = np.asarray(connectivity.elem_plus, dtype=np.int64)
+    src = np.stack([em, ep], axis=1).reshape(-1)
+    dst = np.stack([ep, em], axis=1).reshape(-1)
+    order = np.argsort(src, kind="stable")
+    nbr_flat = dst[order]
+    start = np.zeros(k + 1, dtype=np.int64)
+    np.add.at(start, src + 1, 1)
+    start = np.cumsum(start)
+    neighbors = [nbr_flat[start[i]:start[i + 1]].tolist() for i in range(k)]
+
+    taken = np.zeros(k, dtype=bool)
+    min_free = 0
+    partition = []
+    next_seed = None
+    shared = np.zeros(k, dtype=np.int64)     # faces shared with the current block
+    while min_free < k:
+        seed = next_seed if next_seed is not None and not taken[next_seed] else min_free
+        next_seed = None
+        q_elem = [seed]                      # the queue: append-only, entries popped by flag
+        q_live = [True]
+        live_count = 1
+        entries: dict = {seed: [0]}          # element -> its queue positions
+        heap = [(0, 0)]
+        block = []
+        touched = []
+        while True:
+            while True:                      # the live entry with the most shared faces, earliest
+                neg, pos = heapq.heappop(heap)
+                if q_live[pos] and -neg == shared[q_elem[pos]]:
+                    break
+            elem = q_elem[pos]
+            q_live[pos] = False
+            live_count -= 1
+            if not taken[elem]:
+                taken[elem] = True
+                while min_free < k and taken[min_free]:
+                    min_free += 1
+                block.append(elem)
+                if len(block) == max_block_size:
+                    if live_count:
+                        next_seed = next(q_elem[p] for p in range(len(q_elem)) if q_live[p])
+                    break
+                for nb in neighbors[elem]:  # counts of queued candidates adjacent to elem grow
+                    shared[nb] += 1
+                    touched.append(nb)
+                    for p in entries.get(nb, ()):
+                        if q_live[p]:
+                            heapq.heappush(heap, (-shared[nb], p))
+                for nb in neighbors[elem]:  # queue.extend(neighbors[elem])
+                    p = len(q_elem)
+                    q_elem.append(nb)
+                    q_live.append(True)
+                    live_count += 1
+                    entries.setdefault(nb, []).append(p)
+                    heapq.heappush(heap, (-shared[nb], p))
+            if not live_count:
+                if min_free >= k:
+                    break
+                p = len(q_elem)
+                q_elem.append(min_free)
+                q_live.append(True)
+                live_count += 1
+                entries.setdefault(min_free, []).append(p)
+                heapq.heappush(heap, (-shared[min_free], p))
+        partition.append(block)
+        for nb in touched:
+            shared[nb] = 0
+    return partition
+
+
+def greedy_block_order(vertices: np.ndarray, elements: np.ndarray, block: int = 64, connectivity=None) -> np.ndarray:
+    """Element order made of the Alg. 2 blocks of ``block`` elements (the tensor kernels' tile size)."""
+    from .mesh import Mesh
+
+    blocks = greedy_partition(Mesh(vertices, elements), block, connectivity)
+    return np.concatenate([np.asarray(b, dtype=np.int64) for b in blocks])

@@ -310,3 +310,24 @@ def test_tetgen_roundtrip_and_errors():
     for node, ele in bad:
         with pytest.raises(MeshFormatError):
             read_tetgen(node, ele)
+
+
+def test_greedy_partition_matches_reference_golden():
+    """ordering.greedy_partition == the reference's Alg. 2 (layout.py:59-117) block for block: golden
+    partitions made by simtdg itself (oracle/make_golden_partition.py), incl. a vertex-shuffled mesh
+    and a two-component mesh (reseeding)."""
+    from paper_0901_1024_b200.ordering import greedy_block_order, greedy_partition
+
+    g = load_golden("partition.npz")
+    for name in ("c1", "shuffled", "two_components"):
+        mesh = Mesh(g[f"{name}_vertices"], g[f"{name}_elements"].astype(np.int64))
+        conn = build_connectivity(mesh)
+        for size in (1, 5, 16, 64):
+            blocks = greedy_partition(mesh, size, conn)
+            assert np.array_equal(np.concatenate(blocks), g[f"{name}_b{size}_order"])
+            assert np.array_equal(np.cumsum([0] + [len(b) for b in blocks]), g[f"{name}_b{size}_offsets"])
+            assert all(1 <= len(b) <= size for b in blocks)
+        order = greedy_block_order(mesh.vertices, mesh.elements, 16, conn)
+        assert np.array_equal(np.sort(order), np.arange(mesh.num_elements))
+    with pytest.raises(ValueError):
+        greedy_partition(generate_box_mesh((1.0, 1.0, 1.0), (1, 1, 1)), 0)

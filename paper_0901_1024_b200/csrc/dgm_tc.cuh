@@ -105,6 +105,14 @@ struct TcCfg {
   static constexpr bool SMALL = false;
 #endif
   static constexpr int MAP = SMALL ? 2 : (N <= 6 ? 0 : (N <= 8 ? 1 : 2));
+  // packed fp32x2 A-operand build and tf32 split (FMUL2 / FFMA2 / FADD2): measured per order against
+  // the scalar form (profiles/r02/ab_f32x2.txt): N=2 -3.6 %, N=3, 5, 6 within 0.6 %, N=4 +5.7 %
+  // (12 B of spills at the 96-register cap); on where it wins, or everywhere with DGM_TC_F32X2
+#ifdef DGM_TC_F32X2
+  static constexpr bool F32X2 = MAP == 0;
+#else
+  static constexpr bool F32X2 = N == 2;
+#endif
   static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? 32 : 16);  // elements per CTA
   static constexpr int MT = MAP == 0 ? 3 : (MAP == 1 ? 2 : 1);     // M-tiles
 #if defined(DGM_TC_WIDE_MASK)
@@ -477,11 +485,26 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
           lds_vec<CW>(s_u + ((fb + 0) * TE + row) * NPG + j0, xs);
           lds_vec<CW>(s_u + ((fb + 1) * TE + row) * NPG + j0, ys);
           lds_vec<CW>(s_u + ((fb + 2) * TE + row) * NPG + j0, zs);
+          if constexpr (T::F32X2) {
+          // packed pairs: v = p_a * a - p_b * b as FMUL2(-p_b, b) then FFMA2(p_a, a, .)
+          const float n0 = -p0, n1 = -p1, n2 = -p2;
+#pragma unroll
+          for (int q = 0; q < CW; q += 2) {  // (curl H) / eps, or -(curl E) / mu via the sign in p
+            float t0, t1;
+            mul2(t0, t1, n2, n2, ys[q], ys[q + 1]);
+            fma2(v[0][q], v[0][q + 1], p1, p1, zs[q], zs[q + 1], t0, t1);
+            mul2(t0, t1, n0, n0, zs[q], zs[q + 1]);
+            fma2(v[1][q], v[1][q + 1], p2, p2, xs[q], xs[q + 1], t0, t1);
+            mul2(t0, t1, n1, n1, xs[q], xs[q + 1]);
+            fma2(v[2][q], v[2][q + 1], p0, p0, ys[q], ys[q + 1], t0, t1);
+          }
+          } else {
 #pragma unroll
           for (int q = 0; q < CW; ++q) {  // (curl H) / eps, or -(curl E) / mu via the sign in p
             v[0][q] = p1 * zs[q] - p2 * ys[q];
             v[1][q] = p2 * xs[q] - p0 * zs[q];
             v[2][q] = p0 * ys[q] - p1 * xs[q];
+          }
           }
         } else if (k >= KV) {
           const int node = (k - KV) % NFPK;
@@ -589,10 +612,18 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #pragma unroll
       for (int j = 0; j < T::KH; ++j) {
         float hi[MT][T::CW], lo[MT][T::CW];
+        if constexpr (T::F32X2) {
 #pragma unroll
-        for (int t = 0; t < MT; ++t)
+          for (int t = 0; t < MT; ++t)
 #pragma unroll
-          for (int q = 0; q < T::CW; ++q) split_tf32(vcur[j][t][q], hi[t][q], lo[t][q]);  // dead rows are 0
+            for (int q = 0; q < T::CW; q += 2)
+              split_tf32_2(vcur[j][t][q], vcur[j][t][q + 1], hi[t][q], hi[t][q + 1], lo[t][q], lo[t][q + 1]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < MT; ++t)
+#pragma unroll
+            for (int q = 0; q < T::CW; ++q) split_tf32(vcur[j][t][q], hi[t][q], lo[t][q]);  // dead rows are 0
+        }
         if (j == 0) {
           mbar_wait(&empty[slot], eph);
           if (tid == 0) TC_TRACE(0, 102 + 4 * s);  // stage free

@@ -456,46 +456,60 @@ stage_kernel(const StageArgs<T> a) {
   }  // SIMT P2
 
   // ---------------- P3: coalesced write-back ----------------
+  // (field, chunk) work items flattened over the CTA; the residual chunks of all of a thread's items
+  // are loaded first (L2-prefetched in P0), so the loads overlap instead of one round trip per field
   {
     constexpr int RV = NPG / VEC;
+    constexpr int PER = (6 * TE * RV + C::THREADS - 1) / C::THREADS;
     const int nvec = nv * RV;
-#pragma unroll 1
-    for (int f = 0; f < 6; ++f) {
-      const int64_t gbase = ((int64_t)f * a.kf + e0) * NPG;
-      for (int c = tid; c < nvec; c += blockDim.x) {
-        const int k = c / RV, jv = c - k * RV;
-        T rh[VEC];
-        const T* srow = s_fl + (f * TE + k) * NFS + jv * VEC;
+    const int total = 6 * nvec;
+    V ro[PER];
+    if (MODE == MODE_LSRK && !a.a_zero) {
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) rh[q] = (jv * VEC + q < NP) ? srow[q] : T(0);
-        const int64_t go = gbase + (int64_t)c * VEC;  // rows are contiguous: k*NPG + jv*VEC
-        if (MODE == MODE_RHS || MODE == MODE_VOLUME) {
-          V o;
-          T* op = reinterpret_cast<T*>(&o);
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) op[q] = rh[q];
-          *reinterpret_cast<V*>(a.out + go) = o;
-        } else {
-          V r;
-          T* rp = reinterpret_cast<T*>(&r);
-          if (a.a_zero) {
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) rp[q] = a.dt * rh[q];
-          } else {
-            const V ro = *reinterpret_cast<const V*>(a.res + go);
-            const T* rop = reinterpret_cast<const T*>(&ro);
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) rp[q] = a.a * rop[q] + a.dt * rh[q];
-          }
-          *reinterpret_cast<V*>(a.res + go) = r;
-          const V uo = *reinterpret_cast<const V*>(s_u + (f * TE + k) * NPG + jv * VEC);
-          const T* uop = reinterpret_cast<const T*>(&uo);
-          V un;
-          T* unp = reinterpret_cast<T*>(&un);
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) unp[q] = uop[q] + a.b * rp[q];
-          *reinterpret_cast<V*>(a.u_out + go) = un;
+      for (int p = 0; p < PER; ++p) {
+        const int idx = tid + p * C::THREADS;
+        if (idx < total) {
+          const int f = idx / nvec, c = idx - f * nvec;
+          ro[p] = *reinterpret_cast<const V*>(a.res + ((int64_t)f * a.kf + e0) * NPG + (int64_t)c * VEC);
         }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int idx = tid + p * C::THREADS;
+      if (idx >= total) break;
+      const int f = idx / nvec, c = idx - f * nvec;
+      const int k = c / RV, jv = c - k * RV;
+      const int64_t go = ((int64_t)f * a.kf + e0) * NPG + (int64_t)c * VEC;  // rows are contiguous
+      T rh[VEC];
+      const T* srow = s_fl + (f * TE + k) * NFS + jv * VEC;
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) rh[q] = (jv * VEC + q < NP) ? srow[q] : T(0);
+      if (MODE == MODE_RHS || MODE == MODE_VOLUME) {
+        V o;
+        T* op = reinterpret_cast<T*>(&o);
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) op[q] = rh[q];
+        *reinterpret_cast<V*>(a.out + go) = o;
+      } else {
+        V r;
+        T* rp = reinterpret_cast<T*>(&r);
+        if (a.a_zero) {
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) rp[q] = a.dt * rh[q];
+        } else {
+          const T* rop = reinterpret_cast<const T*>(&ro[p]);
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) rp[q] = a.a * rop[q] + a.dt * rh[q];
+        }
+        *reinterpret_cast<V*>(a.res + go) = r;
+        const V uo = *reinterpret_cast<const V*>(s_u + (f * TE + k) * NPG + jv * VEC);
+        const T* uop = reinterpret_cast<const T*>(&uo);
+        V un;
+        T* unp = reinterpret_cast<T*>(&un);
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) unp[q] = uop[q] + a.b * rp[q];
+        *reinterpret_cast<V*>(a.u_out + go) = un;
       }
     }
   }

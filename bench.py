@@ -452,7 +452,7 @@ EXTRAS = {
     "C4": dict(order=4, cells=(110, 110, 110), dtype="f32", steps=5, warmup=3, graph=False,
                what="C4 N=4, 7,986,000 tets on one GPU (N=1 point of the strong-scaling series)"),
 }
-DEFAULT_EXTRAS = ("C1", "C2_N1", "C2_N3", "C2_N6", "C2_N9", "C3_f64", "C5")
+DEFAULT_EXTRAS = ("C1", "C2_N1", "C2_N3", "C2_N6", "C2_N9", "C3_f64", "C5", "C4")
 
 
 def run_extra(name, spec, dev, clocks, peaks, pipes, ncu) -> dict:

@@ -229,48 +229,64 @@ stage_kernel(const StageArgs<T> a) {
   __syncthreads();
 
   // ---------------- P1: surface flux ----------------
+  // two work items per round: both items' trace loads (smem, or L2 for out-of-tile neighbours) are
+  // issued before either is used
   if (MODE != MODE_VOLUME) {
     const int nwork = nv * 4 * NFP;
-    for (int w = tid; w < nwork; w += blockDim.x) {
-      const int k = w / (4 * NFP);
-      const int r = w - k * (4 * NFP);
-      const int face = r / NFP;
-      const int node = r - face * NFP;
-      const int im = s_fmask[face * NFP + node];
+    struct Item {
+      int k, r, face, code;
       T um[6], up[6];
+    };
+    auto gather = [&](int w, Item& it) {
+      it.k = w / (4 * NFP);
+      it.r = w - it.k * (4 * NFP);
+      it.face = it.r / NFP;
+      const int node = it.r - it.face * NFP;
+      const int im = s_fmask[it.face * NFP + node];
 #pragma unroll
-      for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + k) * NPG + im];
-      const T* gk = s_geo + k * GEO_WORDS;
-      const T nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
-      const int code = s_code[k * 4 + face];
-      if (code < 0) {
-        // PEC mirror (maxwell.py:117-132)
-        const T nde = nx * um[0] + ny * um[1] + nz * um[2];
-        const T ndh = nx * um[3] + ny * um[4] + nz * um[5];
-        up[0] = -um[0] + T(2) * nde * nx;
-        up[1] = -um[1] + T(2) * nde * ny;
-        up[2] = -um[2] + T(2) * nde * nz;
-        up[3] = um[3] - T(2) * ndh * nx;
-        up[4] = um[4] - T(2) * ndh * ny;
-        up[5] = um[5] - T(2) * ndh * nz;
-      } else {
-        const int nb = s_nbr[k * 4 + face];
-        const int jn = s_ptab[code * NFP + node];
+      for (int f = 0; f < 6; ++f) it.um[f] = s_u[(f * TE + it.k) * NPG + im];
+      it.code = s_code[it.k * 4 + it.face];
+      if (it.code >= 0) {
+        const int nb = s_nbr[it.k * 4 + it.face];
+        const int jn = s_ptab[it.code * NFP + node];
         const int64_t loc = (int64_t)nb - e0;
         if (loc >= 0 && loc < nv) {
 #pragma unroll
-          for (int f = 0; f < 6; ++f) up[f] = s_u[(f * TE + (int)loc) * NPG + jn];
+          for (int f = 0; f < 6; ++f) it.up[f] = s_u[(f * TE + (int)loc) * NPG + jn];
         } else {
           const T* p = a.u + (int64_t)nb * NPG + jn;
 #pragma unroll
-          for (int f = 0; f < 6; ++f) up[f] = __ldg(p + f * fstride);
+          for (int f = 0; f < 6; ++f) it.up[f] = __ldg(p + f * fstride);
         }
       }
+    };
+    auto finish = [&](Item& it) {
+      const T* gk = s_geo + it.k * GEO_WORDS;
+      const T nx = gk[10 + 3 * it.face], ny = gk[11 + 3 * it.face], nz = gk[12 + 3 * it.face];
+      if (it.code < 0) {
+        // PEC mirror (maxwell.py:117-132)
+        const T nde = nx * it.um[0] + ny * it.um[1] + nz * it.um[2];
+        const T ndh = nx * it.um[3] + ny * it.um[4] + nz * it.um[5];
+        it.up[0] = -it.um[0] + T(2) * nde * nx;
+        it.up[1] = -it.um[1] + T(2) * nde * ny;
+        it.up[2] = -it.um[2] + T(2) * nde * nz;
+        it.up[3] = it.um[3] - T(2) * ndh * nx;
+        it.up[4] = it.um[4] - T(2) * ndh * ny;
+        it.up[5] = it.um[5] - T(2) * ndh * nz;
+      }
       T fl[6];
-      upwind(um, up, nx, ny, nz, a, fl);
-      const T sj = gk[22 + face];
+      upwind(it.um, it.up, nx, ny, nz, a, fl);
+      const T sj = gk[22 + it.face];
 #pragma unroll
-      for (int f = 0; f < 6; ++f) s_fl[(f * TE + k) * NFS + r] = fl[f] * sj;
+      for (int f = 0; f < 6; ++f) s_fl[(f * TE + it.k) * NFS + it.r] = fl[f] * sj;
+    };
+    for (int w = tid; w < nwork; w += 2 * blockDim.x) {
+      const int w2 = w + blockDim.x;
+      Item i1, i2;
+      gather(w, i1);
+      if (w2 < nwork) gather(w2, i2);
+      finish(i1);
+      if (w2 < nwork) finish(i2);
     }
     __syncthreads();
   }

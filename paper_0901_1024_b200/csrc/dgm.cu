@@ -226,6 +226,14 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
       return r;
     if ((r = raise_smem_limit(dgm::stage_kernel<N, T, dgm::MODE_SURFACE>, smem, "cudaFuncSetAttribute")))
       return r;
+    if constexpr (sizeof(T) == 4 && N <= 4) {  // the small-tile variant (a few tiles per launch)
+      using CS = dgm::Cfg<N, T, 1>;
+      static_assert(CS::SMEM_FIXED <= C::SMEM_FIXED, "small tiles need less shared memory");
+      if ((r = raise_smem_limit(dgm::stage_kernel<N, T, dgm::MODE_RHS, 1>, smem, "cudaFuncSetAttribute")))
+        return r;
+      if ((r = raise_smem_limit(dgm::stage_kernel<N, T, dgm::MODE_LSRK, 1>, smem, "cudaFuncSetAttribute")))
+        return r;
+    }
     const size_t msmem = (size_t)6 * C::TE * C::NPG * sizeof(T);
     if ((r = raise_smem_limit(dgm::mass_norm_kernel<N, T>, msmem, "cudaFuncSetAttribute")))
       return r;
@@ -476,6 +484,17 @@ int launch_stage(const dgm_plan* plan, const void* u, void* u_out, void* res, vo
       }
     }
     const int64_t tiles = (e_end - e_begin + C::TE - 1) / C::TE;
+    if constexpr (sizeof(T) == 4 && N <= 4 && (MODE == dgm::MODE_RHS || MODE == dgm::MODE_LSRK)) {
+      // fewer tiles than SMs: one element per P2 thread, E times more CTAs with E times shorter
+      // phases (C1, 1,512 tets at N=3: DESIGN.md 3.1)
+      if (tiles < plan->num_sms) {
+        using CS = dgm::Cfg<N, T, 1>;
+        const int64_t st = (e_end - e_begin + CS::TE - 1) / CS::TE;
+        dgm::stage_kernel<N, T, MODE, 1><<<(unsigned)st, CS::THREADS, plan->stage_smem,
+                                           static_cast<cudaStream_t>(stream)>>>(args);
+        return cuda_check(cudaGetLastError(), "stage_kernel launch");
+      }
+    }
     dgm::stage_kernel<N, T, MODE><<<(unsigned)tiles, C::THREADS, plan->stage_smem,
                                     static_cast<cudaStream_t>(stream)>>>(args);
     return cuda_check(cudaGetLastError(), "stage_kernel launch");

@@ -45,7 +45,9 @@ __host__ __device__ constexpr int odd_chunk_pad(int n, int w) {
   return m;
 }
 
-template <int N, typename T>
+// SMALL = 1: one element per P2 thread (tiles of G elements) for launches of only a few tiles,
+// where the per-tile latency, not the throughput, sets the stage time (C1: 1,512 tets).
+template <int N, typename T, int SMALL = 0>
 struct Cfg {
   static constexpr int NP = np_of(N);
   static constexpr int NFP = nfp_of(N);
@@ -65,7 +67,7 @@ struct Cfg {
   // with tiles of 16 elements (two 8-column MMA tiles): N=6 as 4 groups x 4 elements
   static constexpr bool F64N6 = W == 8 && N == 6;
   static constexpr int G = F64N6 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
-  static constexpr int E = F64N6 ? 4 : ((W == 4) ? 4 : 2);
+  static constexpr int E = SMALL ? 1 : (F64N6 ? 4 : ((W == 4) ? 4 : 2));
 #endif
   static constexpr int TE = G * E;                           // elements per tile
   static constexpr int WORK = NP * G;
@@ -74,7 +76,7 @@ struct Cfg {
 #ifdef DGM_F64_SIMT_P2
   static constexpr bool DMMA = false;
 #else
-  static constexpr bool DMMA = W == 8 && N <= 6 && TE % 8 == 0;
+  static constexpr bool DMMA = W == 8 && N <= 6 && TE % 8 == 0 && !SMALL;
 #endif
   static constexpr int NIT = (NP + 7) / 8;                   // DMMA node tiles
   static constexpr int DTASKS = NIT * (TE / 8) * 2;
@@ -166,10 +168,10 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int N, typename T, int MODE>
-__global__ void __launch_bounds__(Cfg<N, T>::THREADS, Cfg<N, T>::MIN_BLOCKS)
+template <int N, typename T, int MODE, int SMALL = 0>
+__global__ void __launch_bounds__(Cfg<N, T, SMALL>::THREADS, Cfg<N, T, SMALL>::MIN_BLOCKS)
 stage_kernel(const StageArgs<T> a) {
-  using C = Cfg<N, T>;
+  using C = Cfg<N, T, SMALL>;
   using V = typename V16<T>::type;
   constexpr int TE = C::TE, NPG = C::NPG, NFS = C::NFS, NP = C::NP, NFP = C::NFP;
   constexpr int VEC = C::VEC, G = C::G, E = C::E;

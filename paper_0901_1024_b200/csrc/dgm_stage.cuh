@@ -197,11 +197,15 @@ stage_kernel(const StageArgs<T> a) {
   __shared__ __align__(8) uint64_t s_bar;
   {
     constexpr int RV = NPG / VEC;  // 16-byte chunks per u row
+    // programmatic dependent launch: the next stage's grid may be scheduled now; this one touches the
+    // state only after its predecessor completed (griddepcontrol.wait)
+    tc::griddep_launch();
     if (tid == 0) {
       tc::mbar_init(&s_bar, 1);
       tc::mbar_init_fence();
     }
     __syncthreads();
+    tc::griddep_wait();
     if (tid == 0) {
       const uint32_t rowb = (uint32_t)nv * NPG * sizeof(T), geob = (uint32_t)nv * GEO_WORDS * sizeof(T);
       const uint32_t conb = (uint32_t)nv * 16;

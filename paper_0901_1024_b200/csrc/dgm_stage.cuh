@@ -64,10 +64,12 @@ struct Cfg {
   static constexpr int E = W == 8 ? DGM_SIMT_E64 : 4;
 #else
   // element groups x elements per thread (SIMT P2 and the mass norm); fp64 N <= 6 runs P2 on DMMA
-  // with tiles of 16 elements (two 8-column MMA tiles): N=6 as 4 groups x 4 elements
-  static constexpr bool F64N6 = W == 8 && N == 6;
-  static constexpr int G = F64N6 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
-  static constexpr int E = SMALL ? 1 : (F64N6 ? 4 : ((W == 4) ? 4 : 2));
+  // fp64 DMMA tiles of 8 elements (one MMA column tile), two tasks per warp, up to 4 CTAs per SM so
+  // one CTA's flux / write-back phases overlap others' DMMA phases: C3 fp64 4.17 -> 3.96 ms per stage,
+  // C2 fp64 N=3, 5, 6 -13..15 % (profiles/r02/ab_f64_te8.txt; 3 CTAs per SM measured slower at N=4)
+  static constexpr bool T8 = W == 8 && N <= 6;
+  static constexpr int G = T8 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
+  static constexpr int E = SMALL ? 1 : (T8 ? 2 : ((W == 4) ? 4 : 2));
 #endif
   static constexpr int TE = G * E;                           // elements per tile
   static constexpr int WORK = NP * G;
@@ -80,7 +82,7 @@ struct Cfg {
 #endif
   static constexpr int NIT = (NP + 7) / 8;                   // DMMA node tiles
   static constexpr int DTASKS = NIT * (TE / 8) * 2;
-  static constexpr int DWARPS = DTASKS < 10 ? DTASKS : 10;
+  static constexpr int DWARPS = T8 ? (DTASKS + 1) / 2 : (DTASKS < 10 ? DTASKS : 10);
   static constexpr int THREADS_SIMT = ((WORK + 31) / 32) * 32;
   static constexpr int THREADS = (DMMA && 32 * DWARPS > THREADS_SIMT) ? 32 * DWARPS : THREADS_SIMT;
   static_assert(NF4 >= NP, "rhs rows reuse the flux buffer");
@@ -89,7 +91,8 @@ struct Cfg {
   // Two CTAs per SM when shared memory allows it and N <= 6: capping registers there costs
   // <= 220 B of spills and gains 1.1-1.5x (profiles/r01/simt_minblocks.json); at N >= 7 the
   // spills (300-400 B) cost more than the occupancy gains.
-  static constexpr int MIN_BLOCKS = (N <= 6 && 2 * (SMEM_FIXED + 2048) <= 227 * 1024) ? 2 : 1;
+  static constexpr int MIN_BLOCKS = T8 ? (4 * (SMEM_FIXED + 2048) <= 227 * 1024 ? 4 : 2)
+                                       : ((N <= 6 && 2 * (SMEM_FIXED + 2048) <= 227 * 1024) ? 2 : 1);
 };
 
 template <typename T> struct V16;
@@ -237,7 +240,11 @@ stage_kernel(const StageArgs<T> a) {
   // ---------------- P1: surface flux ----------------
   // two work items per round: both items' trace loads (smem, or L2 for out-of-tile neighbours) are
   // issued before either is used
+#ifdef DGM_EXP_NOP1
+  if (false) {
+#else
   if (MODE != MODE_VOLUME) {
+#endif
     const int nwork = nv * 4 * NFP;
     struct Item {
       int k, r, face, code;
@@ -333,6 +340,7 @@ stage_kernel(const StageArgs<T> a) {
         for (int t = 0; t < 3; ++t) acc[mu][t][0] = acc[mu][t][1] = T(0);
 #pragma unroll
       for (int t = 0; t < 3; ++t) accl[t][0] = accl[t][1] = T(0);
+#ifndef DGM_EXP_NOP2
 #pragma unroll 3
       for (int k0 = 0; k0 < KJ; k0 += 4) {
         const int k = k0 + t4;
@@ -356,6 +364,7 @@ stage_kernel(const StageArgs<T> a) {
           for (int t = 0; t < 3; ++t) dmma_8x8x4(accl[t], al, s_fl[((3 * (1 - hh) + t) * TE + eb) * NFS + k]);
         }
       }
+#endif
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int e = 8 * eh + 2 * t4 + c;

@@ -69,7 +69,10 @@ struct Cfg {
   // C2 fp64 N=3, 5, 6 -13..15 % (profiles/r02/ab_f64_te8.txt; 3 CTAs per SM measured slower at N=4)
   static constexpr bool T8 = W == 8 && N <= 6;
   static constexpr int G = T8 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
-  static constexpr int E = SMALL ? 1 : (T8 ? 2 : ((W == 4) ? 4 : 2));
+  // fp32 N=2: two elements per thread and up to 4 CTAs per SM (C2 N=2 38.9 -> 35.4 us per stage;
+  // N=1, 3 measured neutral or slower, profiles/r02/ab_simt_f32.txt)
+  static constexpr bool F32N2 = W == 4 && N == 2;
+  static constexpr int E = SMALL ? 1 : ((T8 || F32N2) ? 2 : ((W == 4) ? 4 : 2));
 #endif
   static constexpr int TE = G * E;                           // elements per tile
   static constexpr int WORK = NP * G;
@@ -91,7 +94,7 @@ struct Cfg {
   // Two CTAs per SM when shared memory allows it and N <= 6: capping registers there costs
   // <= 220 B of spills and gains 1.1-1.5x (profiles/r01/simt_minblocks.json); at N >= 7 the
   // spills (300-400 B) cost more than the occupancy gains.
-  static constexpr int MIN_BLOCKS = T8 ? (4 * (SMEM_FIXED + 2048) <= 227 * 1024 ? 4 : 2)
+  static constexpr int MIN_BLOCKS = (T8 || F32N2) ? (4 * (SMEM_FIXED + 2048) <= 227 * 1024 ? 4 : 2)
                                        : ((N <= 6 && 2 * (SMEM_FIXED + 2048) <= 227 * 1024) ? 2 : 1);
 };
 

@@ -25,5 +25,6 @@ cap c2n3 3 "20 20 20" f32
 cap c2n6 6 "20 20 20" f32
 cap c2n9 9 "20 20 20" f32
 cap c1 3 "6 6 7" f32
+cap c4 4 "110 110 110" f32
 du -sh $O
 echo done

@@ -512,12 +512,18 @@ def run_b200(args) -> None:
     from paper_0901_1024_b200.perfmodel import bytes_per_element_stage, dofs, flops_per_element_stage
 
     world, rank, local = _dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # DGM_BENCH_ONE_GPU=1 (testing only): every rank on device 0, to exercise the N > 1 path on a
+    # single-GPU box (NCCL permitting); never set for a reported number
+    gpu = 0 if os.environ.get("DGM_BENCH_ONE_GPU") == "1" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if os.environ.get("DGM_BENCH_ONE_GPU") == "1":  # testing the N > 1 path on one GPU: gloo
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     dtype = torch.float64 if args.dtype == "f64" else torch.float32
     word = 8 if dtype == torch.float64 else 4
     cells = tuple(args.cells)
@@ -593,7 +599,7 @@ def run_b200(args) -> None:
              "tf32": measure_tf32_tflops(dev, sm_max), "fp64": measure_fp64_tflops(dev)}
     ncu = _ncu_summary()
 
-    with ClockSampler(local) as clocks:
+    with ClockSampler(gpu) as clocks:
         # ---- device-resident throughput (value) ----
         advance(u, args.warmup)
         torch.cuda.synchronize()

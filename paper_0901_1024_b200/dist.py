@@ -347,11 +347,24 @@ class DistributedMaxwellOperator:
         self.comm_stream.wait_stream(compute)
         with torch.cuda.stream(self.comm_stream):
             sends = self.pack(u, self.comm_stream)
-            ops = [dist.P2POp(dist.isend, buf, peer) for peer, buf in sends.items()]
-            ops += [dist.P2POp(dist.irecv, buf, peer) for peer, buf in self._recv.items()]
-            if ops:
-                for req in dist.batch_isend_irecv(ops):
-                    req.wait()
+            if dist.is_initialized() and dist.get_backend() == "gloo":
+                # gloo moves host tensors only: stage the (small) trace buffers through the host.  For
+                # tests of the multi-rank paths on one GPU (NCCL refuses two ranks on one device).
+                self.comm_stream.synchronize()
+                host_recv = {p: torch.empty(b.shape, dtype=b.dtype) for p, b in self._recv.items()}
+                ops = [dist.P2POp(dist.isend, buf.cpu(), peer) for peer, buf in sends.items()]
+                ops += [dist.P2POp(dist.irecv, buf, peer) for peer, buf in host_recv.items()]
+                if ops:
+                    for req in dist.batch_isend_irecv(ops):
+                        req.wait()
+                for peer, buf in host_recv.items():
+                    self._recv[peer].copy_(buf)
+            else:
+                ops = [dist.P2POp(dist.isend, buf, peer) for peer, buf in sends.items()]
+                ops += [dist.P2POp(dist.irecv, buf, peer) for peer, buf in self._recv.items()]
+                if ops:
+                    for req in dist.batch_isend_irecv(ops):
+                        req.wait()
             self.unpack(u, self.comm_stream)
             ev = torch.cuda.Event()
             ev.record(self.comm_stream)

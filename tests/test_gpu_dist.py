@@ -237,3 +237,34 @@ def test_nccl_two_ranks_match_single_operator():
     for _, (g0, g1), block in parts:
         got[:, g0:g1] = block
     assert rel_l2(got, want) < 1e-6
+
+
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_multi_rank_path_on_one_gpu(scaling):
+    """bench.py's N > 1 path end to end (torchrun, 2 ranks, DistributedMaxwellOperator, halo exchange,
+    max-over-ranks timing, e2e): both ranks on GPU 0 over gloo (DGM_BENCH_ONE_GPU=1; NCCL refuses two
+    ranks on one device).  Checks the JSON line only -- the numbers of a shared GPU mean nothing."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, DGM_BENCH_ONE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--cells", "12", "10", "10", "--scaling", scaling]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 prints one line
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["value"] > 0 and d["e2e"]["value"] > 0
+    k = 12 * 10 * 10 * 6
+    assert d["config"]["global_elements"] == (k if scaling == "strong" else 2 * k)

@@ -213,7 +213,7 @@ int dgm_plan_create(const dgm_desc* desc, dgm_plan** out) {
     constexpr int N = decltype(n)::value;
     using T = decltype(t);
     using C = dgm::Cfg<N, T>;
-    smem = C::SMEM_FIXED + (size_t)d.num_codes * C::NFP;
+    smem = C::SMEM_FIXED + (size_t)d.num_codes * C::NFP + 4 * (size_t)C::NP + (size_t)d.num_codes;  // + pair tables
     smem = (smem + 15) & ~size_t(15);
     if (smem > 227 * 1024)
       return fail(DGM_ERR_UNSUPPORTED, "stage kernel needs %zu bytes of shared memory", smem);

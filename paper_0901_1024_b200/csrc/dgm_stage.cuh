@@ -181,6 +181,15 @@ stage_kernel(const StageArgs<T> a) {
   using V = typename V16<T>::type;
   constexpr int TE = C::TE, NPG = C::NPG, NFS = C::NFS, NP = C::NP, NFP = C::NFP;
   constexpr int VEC = C::VEC, G = C::G, E = C::E;
+  // The paper's intra-block face-pair reuse in P1 (both sides of an in-tile face from one evaluation,
+  // PAPER.md:1100-1104): built and parity-tested, but measured slower on B200 (C3 fp64 +10 %, C2 fp32
+  // N=1 +25 %, N=2 +23 %: the per-CTA slot tables, the idle partner items and the scattered second
+  // store cost more than the halved arithmetic; profiles/r02/ab_pairs.txt), so opt-in (-DDGM_PAIRS).
+#ifdef DGM_PAIRS
+  constexpr bool PAIRS = true;
+#else
+  constexpr bool PAIRS = false;
+#endif
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* s_u = reinterpret_cast<T*>(smem_raw);
@@ -190,6 +199,10 @@ stage_kernel(const StageArgs<T> a) {
   int* s_code = s_nbr + TE * 4;
   uint8_t* s_fmask = reinterpret_cast<uint8_t*>(s_code + TE * 4);
   uint8_t* s_ptab = s_fmask + 4 * NFP;
+  // face-pair reuse tables (P1): slot of node n in face f (255: not on f), and the neighbour's face
+  // of each code (the face whose node set the code's row lists)
+  uint8_t* s_slot = s_ptab + a.ncodes * NFP;     // [4][NP]
+  uint8_t* s_codeface = s_slot + 4 * NP;         // [ncodes]
 
   const int tid = threadIdx.x;
   const int64_t e0 = a.e_begin + (int64_t)blockIdx.x * TE;
@@ -236,9 +249,25 @@ stage_kernel(const StageArgs<T> a) {
       for (int c = tid; c < 4 * NFP; c += blockDim.x) s_fmask[c] = a.fmask[c];
       for (int c = tid; c < a.ncodes * NFP; c += blockDim.x) s_ptab[c] = a.ptab[c];
     }
+    if (MODE != MODE_VOLUME && PAIRS)
+      for (int c = tid; c < 4 * NP; c += blockDim.x) s_slot[c] = 255;
     tc::mbar_wait(&s_bar, 0);
   }
   __syncthreads();
+  if (MODE != MODE_VOLUME && PAIRS) {
+    for (int c = tid; c < 4 * NFP; c += blockDim.x) s_slot[(c / NFP) * NP + s_fmask[c]] = (uint8_t)(c % NFP);
+    __syncthreads();
+    for (int c = tid; c < a.ncodes; c += blockDim.x) {
+      int face = 0;
+      for (int f = 0; f < 4; ++f) {
+        bool all = true;
+        for (int i = 0; i < NFP; ++i) all = all && s_slot[f * NP + s_ptab[c * NFP + i]] != 255;
+        if (all) face = f;
+      }
+      s_codeface[c] = (uint8_t)face;
+    }
+    __syncthreads();
+  }
 
   // ---------------- P1: surface flux ----------------
   // two work items per round: both items' trace loads (smem, or L2 for out-of-tile neighbours) are
@@ -250,7 +279,7 @@ stage_kernel(const StageArgs<T> a) {
 #endif
     const int nwork = nv * 4 * NFP;
     struct Item {
-      int k, r, face, code;
+      int k, r, face, code, loc, jn;  // loc: in-tile neighbour row or -1; jn: its node at this slot
       T um[6], up[6];
     };
     auto gather = [&](int w, Item& it) {
@@ -262,11 +291,15 @@ stage_kernel(const StageArgs<T> a) {
 #pragma unroll
       for (int f = 0; f < 6; ++f) it.um[f] = s_u[(f * TE + it.k) * NPG + im];
       it.code = s_code[it.k * 4 + it.face];
+      it.loc = -1;
       if (it.code >= 0) {
         const int nb = s_nbr[it.k * 4 + it.face];
         const int jn = s_ptab[it.code * NFP + node];
         const int64_t loc = (int64_t)nb - e0;
         if (loc >= 0 && loc < nv) {
+          it.loc = (int)loc;
+          it.jn = jn;
+          if (PAIRS && it.loc < it.k) return;  // the pair's first element evaluates both sides
 #pragma unroll
           for (int f = 0; f < 6; ++f) it.up[f] = s_u[(f * TE + (int)loc) * NPG + jn];
         } else {
@@ -277,8 +310,34 @@ stage_kernel(const StageArgs<T> a) {
       }
     };
     auto finish = [&](Item& it) {
+      if (PAIRS && it.loc >= 0 && it.loc < it.k) return;  // written by the pair's first element
       const T* gk = s_geo + it.k * GEO_WORDS;
       const T nx = gk[10 + 3 * it.face], ny = gk[11 + 3 * it.face], nz = gk[12 + 3 * it.face];
+      if (PAIRS && it.loc > it.k) {
+        // both sides of an in-tile face at once (the paper's intra-block pair reuse, PAPER.md:1100-1104;
+        // reference gather.py:153-169): with D = u+ - u-, the neighbour sees -D and -n, so its bracket
+        // is T1 - T2 (E) and -S1 + S2 (H) where this side's is T1 + T2 and S1 + S2
+        const T dex = it.up[0] - it.um[0], dey = it.up[1] - it.um[1], dez = it.up[2] - it.um[2];
+        const T dhx = it.up[3] - it.um[3], dhy = it.up[4] - it.um[4], dhz = it.up[5] - it.um[5];
+        const T nde = nx * dex + ny * dey + nz * dez, ndh = nx * dhx + ny * dhy + nz * dhz;
+        const T t1[3] = {a.zp * (ny * dhz - nz * dhy), a.zp * (nz * dhx - nx * dhz), a.zp * (nx * dhy - ny * dhx)};
+        const T t2[3] = {dex - nx * nde, dey - ny * nde, dez - nz * nde};
+        const T s1[3] = {dhx - nx * ndh, dhy - ny * ndh, dhz - nz * ndh};
+        const T s2[3] = {-a.yp * (ny * dez - nz * dey), -a.yp * (nz * dex - nx * dez), -a.yp * (nx * dey - ny * dex)};
+        const T sj = gk[22 + it.face] * a.inv_2z, sjh = gk[22 + it.face] * a.inv_2y;
+        const int pf = s_codeface[it.code];
+        const T* gp = s_geo + it.loc * GEO_WORDS;
+        const T pj = gp[22 + pf] * a.inv_2z, pjh = gp[22 + pf] * a.inv_2y;
+        const int pr = pf * NFP + s_slot[pf * NP + it.jn];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          s_fl[(c * TE + it.k) * NFS + it.r] = (t1[c] + t2[c]) * sj;
+          s_fl[((c + 3) * TE + it.k) * NFS + it.r] = (s1[c] + s2[c]) * sjh;
+          s_fl[(c * TE + it.loc) * NFS + pr] = (t1[c] - t2[c]) * pj;
+          s_fl[((c + 3) * TE + it.loc) * NFS + pr] = (s2[c] - s1[c]) * pjh;
+        }
+        return;
+      }
       if (it.code < 0) {
         // PEC mirror (maxwell.py:117-132)
         const T nde = nx * it.um[0] + ny * it.um[1] + nz * it.um[2];

@@ -67,7 +67,10 @@ struct Cfg {
   // fp64 DMMA tiles of 8 elements (one MMA column tile), two tasks per warp, up to 4 CTAs per SM so
   // one CTA's flux / write-back phases overlap others' DMMA phases: C3 fp64 4.17 -> 3.96 ms per stage,
   // C2 fp64 N=3, 5, 6 -13..15 % (profiles/r02/ab_f64_te8.txt; 3 CTAs per SM measured slower at N=4)
-  static constexpr bool T8 = W == 8 && N <= 6;
+#ifndef DGM_F64_DMMA_MAXN
+#define DGM_F64_DMMA_MAXN 9  // all orders: N=7, 8, 9 at 48k tets 2.69 / 4.15 / 6.34 -> 1.54 / 3.04 / 4.72 ms per stage
+#endif
+  static constexpr bool T8 = W == 8 && N <= DGM_F64_DMMA_MAXN;
   static constexpr int G = T8 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
   // fp32 N=2: two elements per thread and up to 4 CTAs per SM (C2 N=2 38.9 -> 35.4 us per stage;
   // N=1, 3 measured neutral or slower, profiles/r02/ab_simt_f32.txt)
@@ -77,11 +80,11 @@ struct Cfg {
   static constexpr int TE = G * E;                           // elements per tile
   static constexpr int WORK = NP * G;
   // fp64 volume + LIFT on the FP64 tensor path (mma.sync m8n8k4 f64, DMMA): one warp task = 8 nodes x
-  // 8 elements x one field half; N >= 7 keeps the SIMT P2 (tiles of <= 8 elements there)
+  // 8 elements x one field half (all orders; -DDGM_F64_SIMT_P2 restores the CUDA-core P2)
 #ifdef DGM_F64_SIMT_P2
   static constexpr bool DMMA = false;
 #else
-  static constexpr bool DMMA = W == 8 && N <= 6 && TE % 8 == 0 && !SMALL;
+  static constexpr bool DMMA = W == 8 && N <= DGM_F64_DMMA_MAXN && TE % 8 == 0 && !SMALL;
 #endif
   static constexpr int NIT = (NP + 7) / 8;                   // DMMA node tiles
   static constexpr int DTASKS = NIT * (TE / 8) * 2;
@@ -94,7 +97,8 @@ struct Cfg {
   // Two CTAs per SM when shared memory allows it and N <= 6: capping registers there costs
   // <= 220 B of spills and gains 1.1-1.5x (profiles/r01/simt_minblocks.json); at N >= 7 the
   // spills (300-400 B) cost more than the occupancy gains.
-  static constexpr int MIN_BLOCKS = (T8 || F32N2) ? (4 * (SMEM_FIXED + 2048) <= 227 * 1024 ? 4 : 2)
+  static constexpr int MIN_BLOCKS = (T8 || F32N2) ? (4 * (SMEM_FIXED + 2048) <= 227 * 1024 ? 4
+                                                     : (2 * (SMEM_FIXED + 2048) <= 227 * 1024 && N <= 6 ? 2 : 1))
                                        : ((N <= 6 && 2 * (SMEM_FIXED + 2048) <= 227 * 1024) ? 2 : 1);
 };
 

@@ -71,11 +71,14 @@ struct Cfg {
 #define DGM_F64_DMMA_MAXN 9  // all orders: N=7, 8, 9 at 48k tets 2.69 / 4.15 / 6.34 -> 1.54 / 3.04 / 4.72 ms per stage
 #endif
   static constexpr bool T8 = W == 8 && N <= DGM_F64_DMMA_MAXN;
-  static constexpr int G = T8 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2));
+  // fp64 N=8: 2 groups x 4 elements and <= 12 warps (no spills): 3.04 -> 2.84 ms per stage at 48k tets;
+  // measured +6 % at N=7 and neutral at N=9 (profiles/r02/ab_f64_high_orders.txt)
+  static constexpr bool HI2 = T8 && N == 8;
+  static constexpr int G = HI2 ? 2 : (T8 ? 4 : ((N <= 5) ? 8 : (N <= 7 ? 4 : 2)));
   // fp32 N=2: two elements per thread and up to 4 CTAs per SM (C2 N=2 38.9 -> 35.4 us per stage;
   // N=1, 3 measured neutral or slower, profiles/r02/ab_simt_f32.txt)
   static constexpr bool F32N2 = W == 4 && N == 2;
-  static constexpr int E = SMALL ? 1 : ((T8 || F32N2) ? 2 : ((W == 4) ? 4 : 2));
+  static constexpr int E = SMALL ? 1 : (HI2 ? 4 : ((T8 || F32N2) ? 2 : ((W == 4) ? 4 : 2)));
 #endif
   static constexpr int TE = G * E;                           // elements per tile
   static constexpr int WORK = NP * G;
@@ -88,7 +91,8 @@ struct Cfg {
 #endif
   static constexpr int NIT = (NP + 7) / 8;                   // DMMA node tiles
   static constexpr int DTASKS = NIT * (TE / 8) * 2;
-  static constexpr int DWARPS = T8 ? (DTASKS + 1) / 2 : (DTASKS < 10 ? DTASKS : 10);
+  static constexpr int DTPW = HI2 ? (DTASKS + 11) / 12 : 2;  // DMMA tasks per warp
+  static constexpr int DWARPS = T8 ? (DTASKS + DTPW - 1) / DTPW : (DTASKS < 10 ? DTASKS : 10);
   static constexpr int THREADS_SIMT = ((WORK + 31) / 32) * 32;
   static constexpr int THREADS = (DMMA && 32 * DWARPS > THREADS_SIMT) ? 32 * DWARPS : THREADS_SIMT;
   static_assert(NF4 >= NP, "rhs rows reuse the flux buffer");

@@ -130,7 +130,13 @@ struct TcCfg {
   static constexpr int KH = 8 / CW / NQ;           // column groups per producer thread and K-step
   static constexpr int FB = PWARPS == 16 ? 2 : 4;  // face nodes per flux work unit
   static constexpr int PROD = 32 * PWARPS;         // producer threads
-  static constexpr int THREADS = PROD + 64;        // + MMA warp + loader warp
+#ifdef DGM_TC_MERGE
+  // experiment: the loader's work in the MMA warp at 2 CTAs/SM (9 warps per CTA: 112 registers)
+  static constexpr bool MERGE = !SMALL && N <= 4;  // the CTAS == 2 kernels
+#else
+  static constexpr bool MERGE = false;
+#endif
+  static constexpr int THREADS = PROD + (MERGE ? 32 : 64);  // + MMA warp (+ loader warp)
   static constexpr int ACC_COLS = MT * NB;
   static constexpr int A_COL0 = (ACC_COLS + 31) / 32 * 32;
   static constexpr int A_STAGE_COLS = MT * 16;     // M-tiles x (8 hi + 8 lo)
@@ -288,44 +294,45 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
   const uint32_t tmem = *s_tmem;
   TC_TRACE_DECL;
 
-  if (warp == T::PWARPS + 1) {
-    // ================= loader warp =================
-    // warm L2 with the tile's residual rows, read by the epilogue
-    auto prefetch_res = [&]() {
-      const uint32_t rb = (uint32_t)nv * NPG * 4;
-      for (int f = 0; f < 6; ++f) prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rb);
-    };
-    auto load_b = [&](int i) {  // B operand of the i-th K-step (in this CTA's order) into its ring slot
-      if (i >= KS) return;
-      const int slot = i % NBS;
-      const int step = (i + rot) % KS;
-      mbar_expect_tx(&b_full[slot], T::B_STEP_BYTES);
-      bulk_g2s(s_b + slot * T::B_STEP_BYTES, args.bpack + (size_t)step * (T::B_STEP_BYTES / 4), T::B_STEP_BYTES,
-               &b_full[slot]);
-    };
-    if (elect_one()) {
-      for (int i = 0; i < NBS; ++i) load_b(i);
-      const uint32_t rowbytes = (uint32_t)nv * NPG * 4;
-      const uint32_t geobytes = (uint32_t)nv * GEO_WORDS * 4, conbytes = (uint32_t)nv * 16;
-      mbar_expect_tx(load_full, 6 * rowbytes + geobytes + 2 * conbytes);
-      bulk_g2s(s_geo, a.geo + e0 * GEO_WORDS, geobytes, load_full);
-      bulk_g2s(s_nbr, a.nbr + e0 * 4, conbytes, load_full);
-      bulk_g2s(s_code, a.code + e0 * 4, conbytes, load_full);
-      griddep_wait();  // everything above is constant; the state below is the previous stage's output
-      for (int f = 0; f < 6; ++f)
-        bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowbytes, load_full);
-      if (MODE == MODE_LSRK && !a.a_zero && KS <= NBS) prefetch_res();
-      // warm L2 with the rows of the tile one wave ahead, so that CTA's bulk loads hit L2
-      const int64_t nt = (int64_t)blockIdx.x + args.wave;
-      if (nt < args.num_tiles) {
-        const int64_t n0 = a.e_begin + nt * TE;
-        const uint32_t nn = (uint32_t)min((int64_t)TE, a.e_end - n0);
-        for (int f = 0; f < 6; ++f) prefetch_l2(a.u + (int64_t)f * fstride + n0 * NPG, nn * NPG * 4);
-        prefetch_l2(a.geo + n0 * GEO_WORDS, nn * GEO_WORDS * 4);
-        prefetch_l2(a.nbr + n0 * 4, nn * 16);
-        prefetch_l2(a.code + n0 * 4, nn * 16);
-      }
+  auto prefetch_res = [&]() {  // warm L2 with the tile's residual rows, read by the epilogue
+    const uint32_t rb = (uint32_t)nv * NPG * 4;
+    for (int f = 0; f < 6; ++f) prefetch_l2(a.res + (int64_t)f * fstride + e0 * NPG, rb);
+  };
+  auto load_b = [&](int i) {  // B operand of the i-th K-step (in this CTA's order) into its ring slot
+    if (i >= KS) return;
+    const int slot = i % NBS;
+    const int step = (i + rot) % KS;
+    mbar_expect_tx(&b_full[slot], T::B_STEP_BYTES);
+    bulk_g2s(s_b + slot * T::B_STEP_BYTES, args.bpack + (size_t)step * (T::B_STEP_BYTES / 4), T::B_STEP_BYTES,
+             &b_full[slot]);
+  };
+  // the tile's rows, geometry and connectivity, the first NBS B slots, L2 warm-up of the next wave
+  auto load_tile = [&]() {
+    for (int i = 0; i < NBS; ++i) load_b(i);
+    const uint32_t rowbytes = (uint32_t)nv * NPG * 4;
+    const uint32_t geobytes = (uint32_t)nv * GEO_WORDS * 4, conbytes = (uint32_t)nv * 16;
+    mbar_expect_tx(load_full, 6 * rowbytes + geobytes + 2 * conbytes);
+    bulk_g2s(s_geo, a.geo + e0 * GEO_WORDS, geobytes, load_full);
+    bulk_g2s(s_nbr, a.nbr + e0 * 4, conbytes, load_full);
+    bulk_g2s(s_code, a.code + e0 * 4, conbytes, load_full);
+    griddep_wait();  // everything above is constant; the state below is the previous stage's output
+    for (int f = 0; f < 6; ++f)
+      bulk_g2s(s_u + f * TE * NPG, a.u + (int64_t)f * fstride + e0 * NPG, rowbytes, load_full);
+    if (MODE == MODE_LSRK && !a.a_zero && KS <= NBS) prefetch_res();
+    const int64_t nt = (int64_t)blockIdx.x + args.wave;
+    if (nt < args.num_tiles) {
+      const int64_t n0 = a.e_begin + nt * TE;
+      const uint32_t nn = (uint32_t)min((int64_t)TE, a.e_end - n0);
+      for (int f = 0; f < 6; ++f) prefetch_l2(a.u + (int64_t)f * fstride + n0 * NPG, nn * NPG * 4);
+      prefetch_l2(a.geo + n0 * GEO_WORDS, nn * GEO_WORDS * 4);
+      prefetch_l2(a.nbr + n0 * 4, nn * 16);
+      prefetch_l2(a.code + n0 * 4, nn * 16);
     }
+  };
+
+  if (!T::MERGE && warp == T::PWARPS + 1) {
+    // ================= loader warp =================
+    if (elect_one()) load_tile();
     __syncwarp();
     // Refill B slot j % NBS with K-step j + NBS once the MMAs of step j completed.  b_empty[slot]
     // cannot run a phase ahead of this wait: its next completion needs B(j + NBS), loaded below.
@@ -339,10 +346,28 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       __syncwarp();
     }
   } else if (warp == T::PWARPS) {
-    // ================= MMA warp =================
+    // ================= MMA warp (+ the loader's work when MERGE) =================
     const uint32_t idesc = idesc_tf32(128, NB);
+    int jr = 0;  // MERGE: next B refill (slot of K-step jr -> K-step jr + NBS)
+    if constexpr (T::MERGE) {
+      if (elect_one()) load_tile();
+      __syncwarp();
+    }
     for (int s = 0; s < KS; ++s) {  // s: position in this CTA's K order
       const int slot = s % AST;
+      if constexpr (T::MERGE) {
+        // refill every slot whose MMAs are done (non-blocking), and block only when step s's own
+        // slot has not been refilled yet
+        while (jr + NBS < KS && jr < s && (jr + NBS <= s || mbar_test(&b_empty[jr % NBS], (jr / NBS) & 1))) {
+          mbar_wait(&b_empty[jr % NBS], (jr / NBS) & 1);
+          if (elect_one()) {
+            load_b(jr + NBS);
+            if (MODE == MODE_LSRK && !a.a_zero && jr + NBS == KS - 1) prefetch_res();
+          }
+          __syncwarp();
+          ++jr;
+        }
+      }
       mbar_wait(&b_full[s % NBS], (s / NBS) & 1);
       TC_TRACE(1, 700 + s);  // B(s) landed
       mbar_wait(&full[slot], (s / AST) & 1);
@@ -600,7 +625,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     // slot = i % AST, its empty-barrier parity ((i / AST) & 1) ^ 1 and the K-step s = (i + rot) % KS:
     // kept as incremental counters where registers allow (1 CTA/SM: N=6 -3.3 %, N=8 -4.8 %), recomputed
     // per step at 2 CTAs/SM, where the three extra live registers spill at the 96-register cap (+5.6 %)
-    constexpr bool INC = T::CTAS == 1;
+    constexpr bool INC = T::CTAS == 1 || T::MERGE;
     int slot_c = 0, s_c = rot;
     uint32_t eph_c = 1;
     for (int i = 0; i < KS; ++i) {  // i: position in this CTA's K order, s: K-step

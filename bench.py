@@ -409,7 +409,8 @@ def roofline(order, word, path, k, launch_s, peaks, pipes, kernel, traffic):
             "peak": peaks["hbm_gbs"] if hbm else p / 1e12,
             "unit": "GB/s" if hbm else "TFLOP/s",
             "frac": max(t_mem, t_cmp) / launch_s,
-            "traffic": traffic,
+            "traffic": traffic["bytes_per_launch"] if traffic else None,  # ncu DRAM bytes per launch
+            "traffic_source": traffic,
             "kernel": kernel, "path": path, "launch_us": launch_s * 1e6,
             "t_roof_us": max(t_mem, t_cmp) * 1e6, "hbm_term_us": t_mem * 1e6, "compute_term_us": t_cmp * 1e6,
             "hbm_frac": t_mem / launch_s, "compute_frac": t_cmp / launch_s,

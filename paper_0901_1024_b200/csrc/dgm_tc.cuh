@@ -105,6 +105,12 @@ struct TcCfg {
   static constexpr bool SMALL = false;
 #endif
   static constexpr int MAP = SMALL ? 2 : (N <= 6 ? 0 : (N <= 8 ? 1 : 2));
+#ifdef DGM_TC_INLINE_FLUX
+  // experiment: each producer computes its own face values inside the K-loop (no flux passes)
+  static constexpr bool INLINE_FLUX = MAP == 0;
+#else
+  static constexpr bool INLINE_FLUX = false;
+#endif
   // packed fp32x2 A-operand build and tf32 split (FMUL2 / FFMA2 / FADD2): measured per order against
   // the scalar form (profiles/r02/ab_f32x2.txt): N=2 -3.6 %, N=3, 5, 6 within 0.6 %, N=4 +5.7 %
   // (12 B of spills at the 96-register cap); on where it wins, or everywhere with DGM_TC_F32X2
@@ -531,6 +537,60 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
             v[2][q] = p0 * ys[q] - p1 * xs[q];
           }
           }
+        } else if (k >= KV && T::INLINE_FLUX) {
+          // this thread's own flux values (its element row, its half's 3 components, its 4 slots),
+          // no staging: upwind bracket x face scale straight into the A operand (maxwell.py:73-132)
+          const int face = (k - KV) / NFPK, node0 = (k - KV) % NFPK;
+          const int code = row_ok ? s_code[row * 4 + face] : -1;
+          const int nb = s_nbr[row * 4 + face];
+          const float* gk = s_geo + row * GEO_WORDS;
+          const float nx = gk[10 + 3 * face], ny = gk[11 + 3 * face], nz = gk[12 + 3 * face];
+          const float sc = row_ok ? gk[22 + face] * gk[9] : 0.f;
+          const float scale = h == 0 ? sc * a.inv_eps * a.inv_2z : sc * a.inv_mu * a.inv_2y;
+          const int64_t loc = (int64_t)nb - e0;
+          const bool inl = code >= 0 && loc >= 0 && loc < nv;
+#pragma unroll
+          for (int q = 0; q < CW; ++q) {
+            const int slot = node0 + q;
+            const bool real = slot < NFP;
+            const int nd = real ? slot : 0;
+            const int im = s_fmask[face * NFP + nd];
+            const int jn = code >= 0 ? s_ptab[code * NFP + nd] : 0;
+            float um[6], up[6];
+#pragma unroll
+            for (int f = 0; f < 6; ++f) um[f] = s_u[(f * TE + row) * NPG + im];
+            if (inl) {
+#pragma unroll
+              for (int f = 0; f < 6; ++f) up[f] = s_u[(f * TE + (int)loc) * NPG + jn];
+            } else if (code >= 0) {
+              const float* g = a.u + (int64_t)nb * NPG + jn;
+#pragma unroll
+              for (int f = 0; f < 6; ++f) up[f] = __ldg(g + f * fstride);
+            } else {  // PEC mirror (maxwell.py:117-132)
+              const float nde = nx * um[0] + ny * um[1] + nz * um[2];
+              const float ndh = nx * um[3] + ny * um[4] + nz * um[5];
+              up[0] = -um[0] + 2.f * nde * nx;
+              up[1] = -um[1] + 2.f * nde * ny;
+              up[2] = -um[2] + 2.f * nde * nz;
+              up[3] = um[3] - 2.f * ndh * nx;
+              up[4] = um[4] - 2.f * ndh * ny;
+              up[5] = um[5] - 2.f * ndh * nz;
+            }
+            const float dex = up[0] - um[0], dey = up[1] - um[1], dez = up[2] - um[2];
+            const float dhx = up[3] - um[3], dhy = up[4] - um[4], dhz = up[5] - um[5];
+            const float w = real ? scale : 0.f;
+            if (h == 0) {  // E components: Z+ (n x [[H]]) + [[E]] - n (n . [[E]])
+              const float nde = nx * dex + ny * dey + nz * dez;
+              v[0][q] = (a.zp * (ny * dhz - nz * dhy) + (dex - nx * nde)) * w;
+              v[1][q] = (a.zp * (nz * dhx - nx * dhz) + (dey - ny * nde)) * w;
+              v[2][q] = (a.zp * (nx * dhy - ny * dhx) + (dez - nz * nde)) * w;
+            } else {       // H components: [[H]] - n (n . [[H]]) - Y+ (n x [[E]])
+              const float ndh = nx * dhx + ny * dhy + nz * dhz;
+              v[0][q] = ((dhx - nx * ndh) - a.yp * (ny * dez - nz * dey)) * w;
+              v[1][q] = ((dhy - ny * ndh) - a.yp * (nz * dex - nx * dez)) * w;
+              v[2][q] = ((dhz - nz * ndh) - a.yp * (nx * dey - ny * dex)) * w;
+            }
+          }
         } else if (k >= KV) {
           const int node = (k - KV) % NFPK;
 #pragma unroll
@@ -610,7 +670,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
         }
         named_sync(1, PROD);
     };
-    auto face_start = [&](int s) { return s >= KV / 8 && (s - KV / 8) % (NFPK / 8) == 0; };
+    auto face_start = [&](int s) { return !T::INLINE_FLUX && s >= KV / 8 && (s - KV / 8) % (NFPK / 8) == 0; };
 
     // Software-pipelined K loop: the next step's A values are computed between this step's
     // tcgen05.st and its tcgen05.wait::st, hiding the TMEM store latency; a flux pass (two named

@@ -395,6 +395,13 @@ stage_kernel(const StageArgs<T> a) {
     constexpr int MAXT = (NT + NWARPS - 1) / NWARPS;
     constexpr int KJ = (NP + 3) / 4 * 4, NF4 = C::NF4;
     const int warp = tid >> 5, lane = tid & 31, g4 = lane >> 2, t4 = lane & 3;
+    // MMA column n <-> element 8 eh + colp(n): the B-fragment loads (lane: column l/4, K = l%4) of
+    // rows with an odd-16-byte-chunk stride are then conflict-free in each half-warp (rows 0, 2, 4, 6
+    // and 1, 3, 5, 7 sit 8 banks apart); column n = l/4 in natural order was 2-way conflicted.
+    // C3 fp64: shared-load bank conflicts 303 M -> 125 M per launch, 3.960 -> 3.924 ms per stage;
+    // N=3, 5, 6, 8 -0.4..2.0 %, N=9 +1.8 % (its write-back stores conflict more), so N=9 keeps the
+    // natural order (profiles/r02/ab_f64_colp.txt)
+    auto colp = [](int n) { return N <= 8 ? 2 * (n & 3) + (n >> 2) : n; };
     T keep[MAXT][3][2];
 #pragma unroll
     for (int q = 0; q < MAXT; ++q) {
@@ -402,7 +409,7 @@ stage_kernel(const StageArgs<T> a) {
       if (task >= NT) break;
       const int hh = task & 1, rest = task >> 1, eh = rest % NEH, it = rest / NEH;
       const int i = 8 * it + g4;   // A row / accumulator row: node
-      const int eb = 8 * eh + g4;  // B column: element
+      const int eb = 8 * eh + colp(g4);  // B column: element
       T acc[3][3][2], accl[3][2];
 #pragma unroll
       for (int mu = 0; mu < 3; ++mu)
@@ -437,7 +444,7 @@ stage_kernel(const StageArgs<T> a) {
 #endif
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int e = 8 * eh + 2 * t4 + c;
+        const int e = 8 * eh + colp(2 * t4 + c);
         const T* gk = s_geo + e * GEO_WORDS;
         // grad_nu F_t = sum_mu rx[mu][nu] dF_t/dr_mu; (curl F)_t = grad_t1 F_t2 - grad_t2 F_t1
         auto grad = [&](int nu, int t) {
@@ -460,7 +467,7 @@ stage_kernel(const StageArgs<T> a) {
 #pragma unroll
         for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int t = 0; t < 3; ++t) s_fl[((3 * (1 - hh) + t) * TE + 8 * eh + 2 * t4 + c) * NFS + i] = keep[q][t][c];
+          for (int t = 0; t < 3; ++t) s_fl[((3 * (1 - hh) + t) * TE + 8 * eh + colp(2 * t4 + c)) * NFS + i] = keep[q][t][c];
       }
     }
     __syncthreads();

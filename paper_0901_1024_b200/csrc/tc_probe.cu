@@ -524,9 +524,47 @@ __global__ void __launch_bounds__(256) probe_dfma_kernel(int iters, double* sink
   if (s == 12345.0) sink[0] = s;
 }
 
+// Both at once: even warps run the DMMA loop, odd warps the DFMA loop (do the two share a pipe?).
+// flop = blocks * (4 * iters * 8 * 512 + 128 * iters * 8 * 2).
+__global__ void __launch_bounds__(256) probe_fp64_mixed_kernel(int iters, double* sink) {
+  if ((threadIdx.x >> 5) & 1) {
+    double c[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) c[q] = 1e-3 * q;
+    const double a = 1.0 + 1e-9 * threadIdx.x, b = 1e-12;
+    for (int r = 0; r < iters; ++r) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c[q] = fma(c[q], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += c[q];
+    if (s == 12345.0) sink[0] = s;
+  } else {
+    double c[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = 0.0;
+    const double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * threadIdx.x;
+    for (int r = 0; r < iters; ++r) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c[q][0]), "+d"(c[q][1])
+                     : "d"(a), "d"(b));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += c[q][0] + c[q][1];
+    if (s == 12345.0) sink[0] = s;
+  }
+}
+
+// tensor: 1 DMMA, 0 DFMA, 2 both in one kernel (alternate warps)
 extern "C" int dgm_probe_fp64_rate(int tensor, int blocks, int iters, double* sink, void* stream) {
   if (blocks < 1 || iters < 1) return -1;
-  if (tensor)
+  if (tensor == 2)
+    probe_fp64_mixed_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(iters, sink);
+  else if (tensor)
     probe_dmma_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(iters, sink);
   else
     probe_dfma_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(iters, sink);

@@ -29,3 +29,18 @@ for _ in range(3):
     best = ms if best is None else min(best, ms)
 out["mma_sync_tf32_tflops"] = blocks * 8 * iters * 8 * 2048 / (best / 1e3) / 1e12
 print(json.dumps(out, indent=1))
+# DMMA and DFMA in one kernel (alternate warps): about the sum of the two rates if they are separate
+# pipes, about either one if they share the FP64 datapath
+lib.dgm_probe_fp64_rate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+sink64 = torch.zeros(1, dtype=torch.float64, device=dev)
+best = None
+for _ in range(3):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    assert lib.dgm_probe_fp64_rate(2, blocks, iters, sink64.data_ptr(), torch.cuda.current_stream().cuda_stream) == 0
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    best = ms if best is None else min(best, ms)
+out["fp64_mixed_tflops"] = blocks * (4 * iters * 8 * 512 + 128 * iters * 8 * 2) / (best / 1e3) / 1e12
+print(json.dumps({"fp64_mixed_tflops": out["fp64_mixed_tflops"]}))

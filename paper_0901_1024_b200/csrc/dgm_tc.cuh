@@ -111,14 +111,6 @@ struct TcCfg {
 #else
   static constexpr bool INLINE_FLUX = false;
 #endif
-  // packed fp32x2 A-operand build and tf32 split (FMUL2 / FFMA2 / FADD2): measured per order against
-  // the scalar form (profiles/r02/ab_f32x2.txt): N=2 -3.6 %, N=3, 5, 6 within 0.6 %, N=4 +5.7 %
-  // (12 B of spills at the 96-register cap); on where it wins, or everywhere with DGM_TC_F32X2
-#ifdef DGM_TC_F32X2
-  static constexpr bool F32X2 = MAP == 0;
-#else
-  static constexpr bool F32X2 = N == 2;
-#endif
   static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? 32 : 16);  // elements per CTA
   static constexpr int MT = MAP == 0 ? 3 : (MAP == 1 ? 2 : 1);     // M-tiles
 #if defined(DGM_TC_WIDE_MASK)
@@ -142,7 +134,27 @@ struct TcCfg {
 #else
   static constexpr bool MERGE = false;
 #endif
-  static constexpr int THREADS = PROD + (MERGE ? 32 : 64);  // + MMA warp (+ loader warp)
+  // Role-based registers at 2 CTAs/SM (setmaxnreg): a 12-warp CTA (warpgroup 2 = MMA, loader and two
+  // idle warps) launches at 80 registers per thread; warpgroup 2 drops to REG_AUX and the producers
+  // rise to REG_PROD = 104 (from the 96 of a 10-warp CTA), which holds the incremental K-step counters
+  // and the packed fp32x2 build without spills: C3 1369 -> 1358 us per stage, N=3 60.7 -> 59.4
+  // (profiles/r02/ab_rreg.txt); -DDGM_TC_NO_RREG restores the 10-warp CTA
+#ifdef DGM_TC_NO_RREG
+  static constexpr bool RREG = false;
+#else
+  static constexpr bool RREG = !SMALL && !MERGE && N <= 4 && PWARPS == 8;
+#endif
+  static constexpr int REG_AUX = 32, REG_PROD = 104;
+  // packed fp32x2 A-operand build and tf32 split (FMUL2 / FFMA2 / FADD2): measured per order against
+  // the scalar form (profiles/r02/ab_f32x2.txt): N=2 -3.6 %, N=3, 5, 6 within 0.6 %, N=4 +5.7 %
+  // (12 B of spills at the 96-register cap); with the role-based registers (104, no spills) N=3 -1.5 %,
+  // N=4 -0.4 %, N=6 +0.6 % (profiles/r02/ab_rreg.txt): on where it wins, everywhere with DGM_TC_F32X2
+#ifdef DGM_TC_F32X2
+  static constexpr bool F32X2 = MAP == 0;
+#else
+  static constexpr bool F32X2 = N == 2 || RREG;
+#endif
+  static constexpr int THREADS = PROD + (MERGE ? 32 : (RREG ? 128 : 64));  // + MMA warp (+ loader warp)
   static constexpr int ACC_COLS = MT * NB;
   static constexpr int A_COL0 = (ACC_COLS + 31) / 32 * 32;
   static constexpr int A_STAGE_COLS = MT * 16;     // M-tiles x (8 hi + 8 lo)
@@ -336,7 +348,11 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     }
   };
 
-  if (!T::MERGE && warp == T::PWARPS + 1) {
+  if (warp >= T::PWARPS + 2) {
+    // idle warps of the role-based register split (warpgroup 2 must be complete)
+    if constexpr (T::RREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(T::REG_AUX));
+  } else if (!T::MERGE && warp == T::PWARPS + 1) {
+    if constexpr (T::RREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(T::REG_AUX));
     // ================= loader warp =================
     if (elect_one()) load_tile();
     __syncwarp();
@@ -352,6 +368,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       __syncwarp();
     }
   } else if (warp == T::PWARPS) {
+    if constexpr (T::RREG) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(T::REG_AUX));
     // ================= MMA warp (+ the loader's work when MERGE) =================
     const uint32_t idesc = idesc_tf32(128, NB);
     int jr = 0;  // MERGE: next B refill (slot of K-step jr -> K-step jr + NBS)
@@ -403,6 +420,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       TC_TRACE(1, 501 + 2 * s);  // issued
     }
   } else {
+    if constexpr (T::RREG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(T::REG_PROD));
     // ================= producers =================
     const int quad = warp & 3;               // TMEM lane quadrant
     const int khalf = warp >> 2;             // which 4 of a K step's 8 columns
@@ -685,7 +703,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
     // slot = i % AST, its empty-barrier parity ((i / AST) & 1) ^ 1 and the K-step s = (i + rot) % KS:
     // kept as incremental counters where registers allow (1 CTA/SM: N=6 -3.3 %, N=8 -4.8 %), recomputed
     // per step at 2 CTAs/SM, where the three extra live registers spill at the 96-register cap (+5.6 %)
-    constexpr bool INC = T::CTAS == 1 || T::MERGE;
+    constexpr bool INC = T::CTAS == 1 || T::MERGE || T::RREG;
     int slot_c = 0, s_c = rot;
     uint32_t eph_c = 1;
     for (int i = 0; i < KS; ++i) {  // i: position in this CTA's K order, s: K-step

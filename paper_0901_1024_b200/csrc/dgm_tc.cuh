@@ -145,6 +145,13 @@ struct TcCfg {
   static constexpr bool RREG = !SMALL && !MERGE && N <= 4 && PWARPS == 8;
 #endif
   static constexpr int REG_AUX = 32, REG_PROD = 104;
+  // flux pass: u+ of in-tile and out-of-tile neighbours through one generic-address load path
+  // (A/B, profiles/r02/ab_generic_up.txt: N=4 -0.35 %, N=5 -0.6 %, N=3 +0.7 %, N=6 +0.9 %)
+#ifdef DGM_TC_GENERIC_UP
+  static constexpr bool GENERIC_UP = true;
+#else
+  static constexpr bool GENERIC_UP = N == 4 || N == 5;
+#endif
   // packed fp32x2 A-operand build and tf32 split (FMUL2 / FFMA2 / FADD2): measured per order against
   // the scalar form (profiles/r02/ab_f32x2.txt): N=2 -3.6 %, N=3, 5, 6 within 0.6 %, N=4 +5.7 %
   // (12 B of spills at the 96-register cap); with the role-based registers (104, no spills) N=3 -1.5 %,
@@ -649,7 +656,20 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
           }
           float up[FB][6];
           const int64_t loc = (int64_t)nb - e0;
-          if (code >= 0 && loc >= 0 && loc < nv) {  // neighbour row in this tile: shared memory
+          if constexpr (T::GENERIC_UP) {
+            // one generic-address gather for in-tile (shared) and out-of-tile (global) neighbours, so
+            // a warp holding both kinds of rows does not run two load paths one after the other
+            if (code >= 0) {
+              const bool in_tile = loc >= 0 && loc < nv;
+              const float* g = in_tile ? s_u + loc * NPG : a.u + (int64_t)nb * NPG;
+              const int64_t fs = in_tile ? (int64_t)TE * NPG : fstride;
+#pragma unroll
+              for (int j = 0; j < FB; ++j)
+#pragma unroll
+                for (int f = 0; f < 6; ++f)
+                  asm volatile("ld.f32 %0, [%1];" : "=f"(up[j][f]) : "l"(g + f * fs + jn[j]));
+            }
+          } else if (code >= 0 && loc >= 0 && loc < nv) {  // neighbour row in this tile: shared memory
 #pragma unroll
             for (int j = 0; j < FB; ++j)
 #pragma unroll

@@ -95,8 +95,8 @@ struct TcCfg {
   // H_t of the 64 elements].  MAP 1 (N = 7, 8, where a 64-element u tile no longer fits in smem):
   // 32 elements per CTA, M-tiles component-major: tile 0 = [E_x | E_y | E_z | H_x], tile 1 =
   // [H_y | H_z | pad | pad] (32 lanes per component).
-  // MAP 2 (N = 9): 16 elements per CTA, one M-tile holding all six components, lane = 16 c + e
-  // (96 of 128 lanes used).
+  // MAP 2 (N = 9): TE = 21 elements per CTA, one M-tile holding all six components, lane = TE c + e
+  // (126 of 128 lanes used).
 #ifdef DGM_TC_N4_SMALL
   // Experiment knob (measured 2.73 ms vs 1.63 ms per C3 stage): N=4 on 16-element CTAs
   // with 4 producer warps (both K halves per thread) and 3 CTAs per SM.
@@ -111,7 +111,14 @@ struct TcCfg {
 #else
   static constexpr bool INLINE_FLUX = false;
 #endif
-  static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? 32 : 16);  // elements per CTA
+  // MAP 2 tile: 21 elements fill 126 of the 128 lanes (16 used 96: C2 N=9 917 -> 816 us per stage,
+  // profiles/r02/ab_map2_te21.txt); DGM_TC_TE9 overrides it for experiments
+#ifdef DGM_TC_TE9
+  static constexpr int TE_MAP2 = SMALL ? 16 : DGM_TC_TE9;
+#else
+  static constexpr int TE_MAP2 = SMALL ? 16 : 21;
+#endif
+  static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? 32 : TE_MAP2);  // elements per CTA
   static constexpr int MT = MAP == 0 ? 3 : (MAP == 1 ? 2 : 1);     // M-tiles
 #if defined(DGM_TC_WIDE_MASK)
   // experiment knob: bit N set -> 16 producer warps with 2 K-columns per thread at order N
@@ -193,7 +200,7 @@ struct TcCfg {
     int rd = 1;
     if (MAP == 2) {
       int addr[32] = {};
-      for (int l = 0; l < 32; ++l) addr[l] = (l >> 4) * NFPK * S + (l & 15);
+      for (int l = 0; l < 32; ++l) addr[l] = (l / TE) * NFPK * S + (l % TE);
       rd = bank_mult(addr, 32);
     }
     return (tot * 64) / warps + rd * 64;
@@ -217,7 +224,7 @@ struct TcCfg {
   static constexpr size_t OFF_GEO = OFF_U + (size_t)6 * ROWS_BYTES;
   static constexpr size_t OFF_NBR = OFF_GEO + (size_t)TE * GEO_WORDS * 4;
   static constexpr size_t OFF_CODE = OFF_NBR + (size_t)TE * 4 * 4;
-  static constexpr size_t OFF_B = OFF_CODE + (size_t)TE * 4 * 4;
+  static constexpr size_t OFF_B = (OFF_CODE + (size_t)TE * 4 * 4 + 127) / 128 * 128;
   static constexpr size_t FLUX_BYTES = (size_t)6 * NFPK * SROW * 4;
   static constexpr size_t EPI_BYTES = (size_t)2 * ROWS_BYTES;
   static constexpr size_t OFF_STAGE = OFF_B + (size_t)NBS * B_STEP_BYTES;
@@ -229,10 +236,16 @@ struct TcCfg {
 
   // component held by TMEM lane (quadrant q, lane l) in M-tile t (>= 6: padding lanes)
   __host__ __device__ static constexpr int comp_of(int t, int q, int l) {
-    return MAP == 0 ? t + 3 * (q >> 1) : (MAP == 1 ? 4 * t + q : 2 * q + (l >> 4));
+    return MAP == 0 ? t + 3 * (q >> 1) : (MAP == 1 ? 4 * t + q : (32 * q + l) / TE);
   }
   // element row of lane (q, l)
-  __host__ __device__ static constexpr int row_of(int q, int l) { return MAP == 0 ? (q & 1) * 32 + l : (MAP == 1 ? l : (l & 15)); }
+  __host__ __device__ static constexpr int row_of(int q, int l) {
+    return MAP == 0 ? (q & 1) * 32 + l : (MAP == 1 ? l : (32 * q + l) % TE);
+  }
+  // MAP 2: quadrant q holds lanes of epilogue phase p's two components (lanes [2p TE, 2p TE + 2 TE))
+  __host__ __device__ static constexpr bool map2_quad_in_phase(int q, int p) {
+    return 32 * q < (2 * p + 2) * TE && 32 * q + 32 > 2 * p * TE;
+  }
   // epilogue phase p moves two components (which = 0, 1) through the rows buffer
   __host__ __device__ static constexpr int epi_comp(int p, int which) { return MAP == 0 ? p + 3 * which : 2 * p + which; }
 };
@@ -829,19 +842,21 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       }
       // quadrant warps holding the phase's components: TMEM lanes -> smem rows [which][row][NPG]
       // (MAP 0: M-tile t, all four quadrants; MAP 1: M-tile t/2, quadrants 2(t%2), 2(t%2)+1)
-      // (MAP 2: the single M-tile, quadrant t: lanes 0-15 component 2t, 16-31 component 2t+1)
+      // (MAP 2: the single M-tile, the quadrants holding lanes [2t TE, 2t TE + 2 TE): components 2t, 2t+1)
       // EPI_SPLIT (N=6): every column group of those quadrants moves a share of the NB / 8 column
       // chunks, up to four tcgen05.ld in flight per wait (N=6 -3.8 %); elsewhere the first column group
       // moves all chunks, one load per wait (the split measured N=4 +1.0 %, N=5 +1.3 %, N=8 +0.7 %,
       // N=9 +1.5 %)
       constexpr bool EPI_SPLIT = N == 6 && T::MAP == 0;
       const bool mover = (EPI_SPLIT || khalf == 0) &&
-                         (T::MAP == 0 || (T::MAP == 1 ? (quad >> 1) == (t & 1) : quad == t));
+                         (T::MAP == 0 || (T::MAP == 1 ? (quad >> 1) == (t & 1) : T::map2_quad_in_phase(quad, t)));
       if constexpr (!EPI_SPLIT) {
        if (mover) {
         const int tile = T::MAP == 0 ? t : (T::MAP == 1 ? t >> 1 : 0);
-        const int slot = T::MAP == 0 ? h : (T::MAP == 1 ? (quad & 1) : (lane >> 4));
-        float* dst = s_stage + (size_t)slot * TE * NPG + row * NPG;
+        // MAP 2: lane 32 quad + lane holds component (32 quad + lane) / TE; only the phase's two store
+        const int slot = T::MAP == 0 ? h : (T::MAP == 1 ? (quad & 1) : (32 * quad + lane) / TE - 2 * t);
+        const bool mine = T::MAP != 2 || (slot >= 0 && slot < 2);
+        float* dst = s_stage + (size_t)(mine ? slot : 0) * TE * NPG + row * NPG;
 #pragma unroll
         for (int c0 = 0; c0 < NB; c0 += 8) {
           float r8[8];
@@ -850,7 +865,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #pragma unroll
           for (int q = 0; q < 8; q += 4) {
             const int i = c0 + q;
-            if (i < NPG) {
+            if (i < NPG && mine) {
               float4 o;
               o.x = (i + 0 < NP) ? r8[q + 0] : 0.f;
               o.y = (i + 1 < NP) ? r8[q + 1] : 0.f;

@@ -92,9 +92,10 @@ struct TcCfg {
   static constexpr int KT = KV + 4 * NFPK;
   static constexpr int KS = KT / 8;                // K steps (one kind::tf32 MMA each)
   // Lane mapping.  MAP 0 (N <= 6): 64 elements per CTA, M-tile t = [E_t of the 64 elements |
-  // H_t of the 64 elements].  MAP 1 (N = 7, 8, where a 64-element u tile no longer fits in smem):
-  // 32 elements per CTA, M-tiles component-major: tile 0 = [E_x | E_y | E_z | H_x], tile 1 =
-  // [H_y | H_z | pad | pad] (32 lanes per component).
+  // H_t of the 64 elements].  MAP 1 (N = 7, 8, where a 64-element u tile no longer fits in smem),
+  // M-tiles component-major: N=8, 32 elements per CTA, tile 0 = [E_x | E_y | E_z | H_x], tile 1 =
+  // [H_y | H_z | pad | pad] (32 lanes per component); N=7, 42 elements, tile 0 = [E_x | E_y | E_z],
+  // tile 1 = [H_x | H_y | H_z] (42 lanes per component, 2 pad lanes).
   // MAP 2 (N = 9): TE = 21 elements per CTA, one M-tile holding all six components, lane = TE c + e
   // (126 of 128 lanes used).
 #ifdef DGM_TC_N4_SMALL
@@ -118,7 +119,17 @@ struct TcCfg {
 #else
   static constexpr int TE_MAP2 = SMALL ? 16 : 21;
 #endif
-  static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? 32 : TE_MAP2);  // elements per CTA
+  // MAP 1 tile at N=7: 42 elements, three components per M-tile (252 of 256 lanes; 32 elements used
+  // 192: C2 N=7 439 -> 384 us per stage, profiles/r02/ab_map1_te42.txt); N=8 has no shared memory for
+  // more than 32.  DGM_TC_TE7 overrides it for experiments
+#ifdef DGM_TC_TE7
+  static constexpr int TE_MAP1 = N == 7 ? DGM_TC_TE7 : 32;
+#else
+  static constexpr int TE_MAP1 = N == 7 ? 42 : 32;
+#endif
+  // MAP 1 with TE != 32: three components per M-tile (tile t = components 3t..3t+2, lane = TE c' + e)
+  static constexpr bool M1C3 = MAP == 1 && TE_MAP1 != 32;
+  static constexpr int TE = MAP == 0 ? 64 : (MAP == 1 ? TE_MAP1 : TE_MAP2);  // elements per CTA
   static constexpr int MT = MAP == 0 ? 3 : (MAP == 1 ? 2 : 1);     // M-tiles
 #if defined(DGM_TC_WIDE_MASK)
   // experiment knob: bit N set -> 16 producer warps with 2 K-columns per thread at order N
@@ -202,6 +213,15 @@ struct TcCfg {
       int addr[32] = {};
       for (int l = 0; l < 32; ++l) addr[l] = (l / TE) * NFPK * S + (l % TE);
       rd = bank_mult(addr, 32);
+    } else if (M1C3) {  // staging reads of the four quadrants (lane 32 q + l: component slot, row)
+      int r4 = 0;
+      for (int q = 0; q < 4; ++q) {
+        int addr[32] = {}, n = 0;
+        for (int l = 0; l < 32; ++l)
+          if ((32 * q + l) / TE < 3) addr[n++] = ((32 * q + l) / TE) * NFPK * S + (32 * q + l) % TE;
+        r4 += n ? bank_mult(addr, n) : 0;
+      }
+      rd = (r4 + 3) / 4;
     }
     return (tot * 64) / warps + rd * 64;
   }
@@ -236,15 +256,31 @@ struct TcCfg {
 
   // component held by TMEM lane (quadrant q, lane l) in M-tile t (>= 6: padding lanes)
   __host__ __device__ static constexpr int comp_of(int t, int q, int l) {
-    return MAP == 0 ? t + 3 * (q >> 1) : (MAP == 1 ? 4 * t + q : (32 * q + l) / TE);
+    return MAP == 0 ? t + 3 * (q >> 1)
+                    : (MAP == 1 ? (M1C3 ? ((32 * q + l) / TE < 3 ? 3 * t + (32 * q + l) / TE : 6) : 4 * t + q)
+                                : (32 * q + l) / TE);
   }
   // element row of lane (q, l)
   __host__ __device__ static constexpr int row_of(int q, int l) {
-    return MAP == 0 ? (q & 1) * 32 + l : (MAP == 1 ? l : (32 * q + l) % TE);
+    return MAP == 0 ? (q & 1) * 32 + l : (MAP == 1 && !M1C3 ? l : (32 * q + l) % TE);
   }
   // MAP 2: quadrant q holds lanes of epilogue phase p's two components (lanes [2p TE, 2p TE + 2 TE))
   __host__ __device__ static constexpr bool map2_quad_in_phase(int q, int p) {
     return 32 * q < (2 * p + 2) * TE && 32 * q + 32 > 2 * p * TE;
+  }
+  // MAP 1: the M-tile from which quadrant q moves epilogue phase p's components, -1 if none (no
+  // quadrant needs both tiles in one phase)
+  __host__ __device__ static constexpr int map1_epi_tile(int p, int q) {
+    for (int which = 0; which < 2; ++which) {
+      const int c = 2 * p + which;
+      if (M1C3) {
+        const int lo = (c % 3) * TE;
+        if (32 * q < lo + TE && 32 * q + 32 > lo) return c / 3;
+      } else if (c % 4 == q) {
+        return c / 4;
+      }
+    }
+    return -1;
   }
   // epilogue phase p moves two components (which = 0, 1) through the rows buffer
   __host__ __device__ static constexpr int epi_comp(int p, int which) { return MAP == 0 ? p + 3 * which : 2 * p + which; }
@@ -848,14 +884,15 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
       // moves all chunks, one load per wait (the split measured N=4 +1.0 %, N=5 +1.3 %, N=8 +0.7 %,
       // N=9 +1.5 %)
       constexpr bool EPI_SPLIT = N == 6 && T::MAP == 0;
+      const int m1tile = T::MAP != 1 ? 0 : (T::M1C3 ? T::map1_epi_tile(t, quad) : ((quad >> 1) == (t & 1) ? t >> 1 : -1));
       const bool mover = (EPI_SPLIT || khalf == 0) &&
-                         (T::MAP == 0 || (T::MAP == 1 ? (quad >> 1) == (t & 1) : T::map2_quad_in_phase(quad, t)));
+                         (T::MAP == 0 || (T::MAP == 1 ? m1tile >= 0 : T::map2_quad_in_phase(quad, t)));
       if constexpr (!EPI_SPLIT) {
        if (mover) {
-        const int tile = T::MAP == 0 ? t : (T::MAP == 1 ? t >> 1 : 0);
-        // MAP 2: lane 32 quad + lane holds component (32 quad + lane) / TE; only the phase's two store
-        const int slot = T::MAP == 0 ? h : (T::MAP == 1 ? (quad & 1) : (32 * quad + lane) / TE - 2 * t);
-        const bool mine = T::MAP != 2 || (slot >= 0 && slot < 2);
+        const int tile = T::MAP == 0 ? t : (T::MAP == 1 ? m1tile : 0);
+        // MAP 1/2: the lane holds component comp_of(tile, quad, lane); only the phase's two store
+        const int slot = T::MAP == 0 ? h : (T::MAP == 1 && !T::M1C3 ? (quad & 1) : T::comp_of(tile, quad, lane) - 2 * t);
+        const bool mine = T::MAP == 0 || (T::MAP == 1 && !T::M1C3) || (slot >= 0 && slot < 2);
         float* dst = s_stage + (size_t)(mine ? slot : 0) * TE * NPG + row * NPG;
 #pragma unroll
         for (int c0 = 0; c0 < NB; c0 += 8) {

@@ -438,14 +438,8 @@ def _traffic(ncu: dict, order: int, word: int, path: str, elements: int):
 EXTRAS = {
     "C1": dict(order=3, cells=(6, 6, 7), dtype="f32", steps=100, warmup=10, graph=True,
                what="C1 PEC cavity N=3, 1,512 tets, 100 LSRK4 steps through the CUDA-graph path (op.advance)"),
-    "C2_N1": dict(order=1, cells=(20, 20, 20), dtype="f32", steps=20, warmup=3, graph=False,
-                  what="C2 order sweep, 48,000 tets, N=1"),
-    "C2_N3": dict(order=3, cells=(20, 20, 20), dtype="f32", steps=20, warmup=3, graph=False,
-                  what="C2 order sweep, 48,000 tets, N=3"),
-    "C2_N6": dict(order=6, cells=(20, 20, 20), dtype="f32", steps=20, warmup=3, graph=False,
-                  what="C2 order sweep, 48,000 tets, N=6"),
-    "C2_N9": dict(order=9, cells=(20, 20, 20), dtype="f32", steps=10, warmup=3, graph=False,
-                  what="C2 order sweep, 48,000 tets, N=9"),
+    **{"C2_N%d" % n: dict(order=n, cells=(20, 20, 20), dtype="f32", steps=20 if n < 9 else 10, warmup=3,
+                          graph=False, what="C2 order sweep, 48,000 tets, N=%d" % n) for n in range(1, 10)},
     "C3_f64": dict(order=4, cells=(55, 55, 55), dtype="f64", steps=10, warmup=3, graph=False,
                    what="C3 N=4, 998,250 tets, fp64 variant (the reference's precision)"),
     "C5": dict(order=6, cells=(70, 70, 70), dtype="f32", steps=10, warmup=3, graph=False,
@@ -453,7 +447,7 @@ EXTRAS = {
     "C4": dict(order=4, cells=(110, 110, 110), dtype="f32", steps=5, warmup=3, graph=False,
                what="C4 N=4, 7,986,000 tets on one GPU (N=1 point of the strong-scaling series)"),
 }
-DEFAULT_EXTRAS = ("C1", "C2_N1", "C2_N3", "C2_N6", "C2_N9", "C3_f64", "C5", "C4")
+DEFAULT_EXTRAS = ("C1",) + tuple("C2_N%d" % n for n in range(1, 10)) + ("C3_f64", "C5", "C4")
 
 
 def run_extra(name, spec, dev, clocks, peaks, pipes, ncu) -> dict:

@@ -20,10 +20,7 @@ cap() {  # name order "cells" dtype keep
 cap c3 4 "55 55 55" f32 keep
 cap c3f64 4 "55 55 55" f64
 cap c5 6 "70 70 70" f32
-cap c2n1 1 "20 20 20" f32
-cap c2n3 3 "20 20 20" f32
-cap c2n6 6 "20 20 20" f32
-cap c2n9 9 "20 20 20" f32
+for n in 1 2 3 4 5 6 7 8 9; do cap c2n$n $n "20 20 20" f32; done
 cap c1 3 "6 6 7" f32
 cap c4 4 "110 110 110" f32
 du -sh $O

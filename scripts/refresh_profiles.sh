@@ -9,8 +9,11 @@ if [ -f $S/bench.json ]; then
   cp $S/ncu_*_summary.csv $S/launches_c3.csv $D/
   python scripts/update_ncu_summary.py "tc_stage_kernel<4>/f32@998250=$D/ncu_c3_summary.csv" \
     "stage_kernel<4>/f64@998250=$D/ncu_c3f64_summary.csv" "tc_stage_kernel<6>/f32@2058000=$D/ncu_c5_summary.csv" \
-    "stage_kernel<1>/f32@48000=$D/ncu_c2n1_summary.csv" "tc_stage_kernel<3>/f32@48000=$D/ncu_c2n3_summary.csv" \
-    "tc_stage_kernel<6>/f32@48000=$D/ncu_c2n6_summary.csv" "tc_stage_kernel<9>/f32@48000=$D/ncu_c2n9_summary.csv" \
+    "stage_kernel<1>/f32@48000=$D/ncu_c2n1_summary.csv" "stage_kernel<2>/f32@48000=$D/ncu_c2n2_summary.csv" \
+    "tc_stage_kernel<3>/f32@48000=$D/ncu_c2n3_summary.csv" "tc_stage_kernel<4>/f32@48000=$D/ncu_c2n4_summary.csv" \
+    "tc_stage_kernel<5>/f32@48000=$D/ncu_c2n5_summary.csv" "tc_stage_kernel<6>/f32@48000=$D/ncu_c2n6_summary.csv" \
+    "tc_stage_kernel<7>/f32@48000=$D/ncu_c2n7_summary.csv" "tc_stage_kernel<8>/f32@48000=$D/ncu_c2n8_summary.csv" \
+    "tc_stage_kernel<9>/f32@48000=$D/ncu_c2n9_summary.csv" \
     "stage_kernel<3>/f32@1512=$D/ncu_c1_summary.csv" "tc_stage_kernel<4>/f32@7986000=$D/ncu_c4_summary.csv"
 fi
 if [ -f $T/pytest_gpu.log ]; then

@@ -245,7 +245,20 @@ struct TcCfg {
   static constexpr size_t OFF_NBR = OFF_GEO + (size_t)TE * GEO_WORDS * 4;
   static constexpr size_t OFF_CODE = OFF_NBR + (size_t)TE * 4 * 4;
   static constexpr size_t OFF_B = (OFF_CODE + (size_t)TE * 4 * 4 + 127) / 128 * 128;
-  static constexpr size_t FLUX_BYTES = (size_t)6 * NFPK * SROW * 4;
+  // Flux staging layout.  Default: [component][face node][row] (row stride SROW), read as scalars.
+  // FT (MAP 0, NFPK = 16, i.e. N = 3, 4): [component][row][4 node chunks of 16 B], the chunk index
+  // XOR-swizzled by bits 1-2 of the row, so the flux pass writes and the A build reads one 16-byte
+  // vector per (component, row, 4 nodes) and both are bank-conflict-free.  C3 1353 -> 1338 us per
+  // stage; N=3 +0.3 % (profiles/r02/ab_flux_layout.txt), so N=4 only (DGM_TC_FT: N=3 too)
+#ifdef DGM_TC_FT
+  static constexpr bool FT = MAP == 0 && NFPK == 16 && FB == 4 && CW == 4;
+#else
+  static constexpr bool FT = MAP == 0 && NFPK == 16 && FB == 4 && CW == 4 && N == 4;
+#endif
+  __host__ __device__ static constexpr int ft_off(int c, int row, int nb) {  // float offset, FT layout
+    return ((c * TE + row) * 4 + (nb ^ ((row >> 1) & 3))) * 4;
+  }
+  static constexpr size_t FLUX_BYTES = FT ? (size_t)6 * TE * 16 * 4 : (size_t)6 * NFPK * SROW * 4;
   static constexpr size_t EPI_BYTES = (size_t)2 * ROWS_BYTES;
   static constexpr size_t OFF_STAGE = OFF_B + (size_t)NBS * B_STEP_BYTES;
   static constexpr size_t OFF_BAR = OFF_STAGE + (FLUX_BYTES > EPI_BYTES ? FLUX_BYTES : EPI_BYTES);
@@ -667,10 +680,18 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
           }
         } else if (k >= KV) {
           const int node = (k - KV) % NFPK;
+          if constexpr (T::FT) {
 #pragma unroll
-          for (int q = 0; q < CW; ++q)
+            for (int t = 0; t < MT; ++t) {
+              const float4 x = *reinterpret_cast<const float4*>(s_stage + T::ft_off(3 * h + t, row, node >> 2));
+              v[t][0] = x.x, v[t][1] = x.y, v[t][2] = x.z, v[t][3] = x.w;
+            }
+          } else {
 #pragma unroll
-            for (int t = 0; t < MT; ++t) v[t][q] = s_stage[((3 * h + t) * NFPK + node + q) * SROW + row];
+            for (int q = 0; q < CW; ++q)
+#pragma unroll
+              for (int t = 0; t < MT; ++t) v[t][q] = s_stage[((3 * h + t) * NFPK + node + q) * SROW + row];
+          }
         } else {
 #pragma unroll
           for (int q = 0; q < CW; ++q)
@@ -730,6 +751,7 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
 #pragma unroll
               for (int f = 0; f < 6; ++f) up[j][f] = __ldg(g + f * fstride + jn[j]);
           }
+          float fo[6][FB];  // FT: the unit's scaled flux values, stored as one vector per component
 #pragma unroll
           for (int j = 0; j < FB; ++j) {
             float um[6];
@@ -749,10 +771,21 @@ __global__ void __launch_bounds__(TcCfg<N>::THREADS, TcCfg<N>::CTAS) tc_stage_ke
             upwind_num(um, up[j], nx, ny, nz, a.zp, a.yp, out);
             const int node = n0 + j;
             const float kse = node < NFP ? se : 0.f, ksh = node < NFP ? sh : 0.f;
+            if constexpr (T::FT) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * kse;
+              for (int c = 0; c < 6; ++c) fo[c][j] = out[c] * (c < 3 ? kse : ksh);
+            } else {
 #pragma unroll
-            for (int c = 3; c < 6; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * ksh;
+              for (int c = 0; c < 3; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * kse;
+#pragma unroll
+              for (int c = 3; c < 6; ++c) s_stage[(c * NFPK + node) * SROW + r] = out[c] * ksh;
+            }
+          }
+          if constexpr (T::FT) {
+#pragma unroll
+            for (int c = 0; c < 6; ++c)
+              *reinterpret_cast<float4*>(s_stage + T::ft_off(c, r, n0 >> 2)) =
+                  make_float4(fo[c][0], fo[c][1], fo[c][2], fo[c][3]);
           }
         }
         named_sync(1, PROD);

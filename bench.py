@@ -654,6 +654,33 @@ def run_b200(args) -> None:
             raise RuntimeError("non-finite e2e energy")
         del dev_nat, ue
 
+        # ---- the RHS-level drop-in, as the reference's own loop calls it (N=1 only) ----
+        # rk4_step(state, t, dt, lambda t, y: op.rhs(y)) on a float64 numpy state: every RHS call
+        # round-trips the state through pageable host memory and the LSRK arithmetic runs in numpy
+        # on the host (stepper.py:49-70 = assemble.py:105-114).  Host wall clock (the host work is the
+        # point), one warm-up RHS call, then `--dropin-steps` dependent steps.
+        dropin = None
+        if world == 1 and args.dropin_steps > 0:
+            from paper_0901_1024_b200.stepper import rk4_step as host_rk4_step
+
+            y = np.array(u0_host, dtype=np.float64)
+            op.rhs(y)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.dropin_steps):
+                y = host_rk4_step(y, 0.0, dt, lambda t, v: op.rhs(v))
+            torch.cuda.synchronize()
+            d_s = time.perf_counter() - t0
+            if not np.isfinite(y).all():
+                raise RuntimeError("non-finite drop-in state")
+            dropin = {"value": flops_per_element_stage(args.order) * k * 5 * args.dropin_steps / d_s / 1e9,
+                      "unit": UNIT, "steps": args.dropin_steps, "ms_per_step": d_s * 1e3 / args.dropin_steps,
+                      "h2d_bytes_per_step": 5 * y.nbytes, "d2h_bytes_per_step": 5 * y.nbytes,
+                      "timing": "host wall clock",
+                      "path": "reference call pattern: rk4_step(numpy float64 state, t, dt, lambda t, y: op.rhs(y)) "
+                              "-- per RHS: pageable H2D, pack, dgm_rhs, unpack, D2H; LSRK arithmetic in numpy"}
+            del y
+
         # ---- the other BASELINE configs on this GPU (N=1 only) ----
         extras = {}
         if world == 1 and args.extras != "none":
@@ -713,6 +740,7 @@ def run_b200(args) -> None:
         "roofline": roofline(args.order, word, path, k, launch_s, peaks, pipes,
                              _kernel_name(args.order, word, path), _traffic(ncu, args.order, word, path, k)),
         "cpu_baseline": cpu,
+        "dropin_rhs": dropin,
         "e2e": {"value": e2e_gflops, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,
                 "host_dtype": str(e2e_dtype).replace("torch.", ""),
@@ -754,6 +782,8 @@ def main(argv=None) -> None:
                     help="extra config rows at N=1: default (%s), all, none, or a comma list of %s"
                          % (",".join(DEFAULT_EXTRAS), ",".join(EXTRAS)))
     ap.add_argument("--e2e-steps", type=int, default=None, help="e2e steps (default: --steps)")
+    ap.add_argument("--dropin-steps", type=int, default=1,
+                    help="steps of the RHS-level drop-in leg (reference call pattern, host numpy LSRK; 0: skip)")
     ap.add_argument("--element-order", choices=("auto", "natural", "morton", "columns", "greedy"), default="auto",
                     help="internal element numbering (ordering.py); auto = Morton where it pays")
     ap.add_argument("--face-slots", choices=("auto", "natural"), default="auto",

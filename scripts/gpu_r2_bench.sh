@@ -7,11 +7,11 @@ O=gpurun_out/r2bench; mkdir -p $O
 timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err
 timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > $O/bench_ref.json 2> $O/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c3.csv \
-  python bench.py --steps 2 --warmup 3 --extras none --no-cpu-baseline --e2e-steps 1 > $O/launch_run.log 2>&1
+  python bench.py --steps 2 --warmup 3 --extras none --no-cpu-baseline --e2e-steps 1 --dropin-steps 0 > $O/launch_run.log 2>&1
 cap() {  # name order "cells" dtype keep
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:stage_kernel -s 6 -c 1 -o $O/prof_$1 \
     python bench.py --order $2 --cells $3 --dtype $4 --steps 1 --warmup 3 --extras none --no-cpu-baseline \
-    --e2e-steps 1 > $O/ncu_$1.log 2>&1
+    --e2e-steps 1 --dropin-steps 0 > $O/ncu_$1.log 2>&1
   ncu -i $O/prof_$1.ncu-rep --page raw --csv > $O/raw_$1.csv 2>/dev/null
   python scripts/ncu_summary.py $O/raw_$1.csv $O/ncu_$1_summary.csv
   rm -f $O/raw_$1.csv

@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Maxwell DG net GFLOP/s & DOF-updates/s per RK4 step (N=4, tets); HBM GB/s"
 UNIT = "GFLOP/s"
+N_FIELDS_E2E = 6  # field slabs (E_x .. H_z) of the natural state, each copied in --e2e-chunks pieces
 ORDER = 4
 CELLS = (55, 55, 55)
 
@@ -618,41 +619,75 @@ def run_b200(args) -> None:
         # The reference user's state lives on the host in float64 (natural (6, K, Np) layout).  Every
         # e2e step uploads the current host state (pinned), packs it, runs one LSRK4 step, unpacks,
         # downloads the new state into the same host buffer -- the next step's input -- plus the
-        # energy scalar.  Steps depend on each other, so nothing overlaps across steps.
+        # energy scalar.  The copies move contiguous pieces (--e2e-chunks per field slab) on their own
+        # streams: the upload of piece p for step i+1 waits for the download of piece p from step i,
+        # and the step's pack waits for all six uploads, so every step still computes on the previous
+        # step's downloaded output; what overlaps is the download of step i with the upload of step i+1
+        # (PCIe is full duplex).  --e2e-serial: one copy per direction, nothing overlapped.
         e2e_steps = max(1, args.steps if args.e2e_steps is None else min(args.steps, args.e2e_steps))
         e2e_dtype = {"f32": torch.float32, "f64": torch.float64}[args.e2e_dtype]
         host = torch.from_numpy(np.ascontiguousarray(u0_host)).to(e2e_dtype).pin_memory()
         e_host = torch.empty(1, dtype=torch.float64).pin_memory()
         dev_nat = torch.empty(host.shape, dtype=e2e_dtype, device=dev)
+        nat = torch.empty(host.shape, dtype=e2e_dtype, device=dev)
         ue = op.empty_state()
         h2d = host.numel() * host.element_size()
         d2h = h2d + 8
+        up_stream, down_stream = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        kb = [round(j * op.num_elements / args.e2e_chunks) for j in range(args.e2e_chunks + 1)]
+        pieces = [(f, kb[j], kb[j + 1]) for f in range(N_FIELDS_E2E) for j in range(args.e2e_chunks)]
+        down_done = [torch.cuda.Event() for _ in pieces]
+        up_done, computed, e2e_begin = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
 
-        def e2e_step():
-            dev_nat.copy_(host, non_blocking=True)                       # H2D of this step's input
+        def e2e_step(first: bool):
+            if args.e2e_serial:
+                dev_nat.copy_(host, non_blocking=True)                   # H2D of this step's input
+            else:
+                with torch.cuda.stream(up_stream):
+                    up_stream.wait_event(e2e_begin)
+                    for p, (f, k0, k1) in enumerate(pieces):
+                        if not first:
+                            up_stream.wait_event(down_done[p])           # step i's piece p has landed
+                        dev_nat[f, k0:k1].copy_(host[f, k0:k1], non_blocking=True)  # H2D of this step's input
+                    up_done.record(up_stream)
+                stream.wait_event(up_done)
             op.to_padded(dev_nat, out=ue)                                # pack (natural -> padded, cast)
             advance(ue, 1)                                               # 5 fused stage launches
-            nat = op.from_padded(ue, e2e_dtype)                          # unpack
+            op.from_padded(ue, e2e_dtype, out=nat)                       # unpack
             energy_dev = op.mass_norm(ue, 1.0, 1.0)                      # per-step energy scalar
-            host.copy_(nat, non_blocking=True)                           # D2H: the next step's input
-            e_host.copy_(energy_dev, non_blocking=True)
+            if args.e2e_serial:
+                host.copy_(nat, non_blocking=True)                       # D2H: the next step's input
+                e_host.copy_(energy_dev, non_blocking=True)
+                return
+            computed.record(stream)
+            with torch.cuda.stream(down_stream):
+                down_stream.wait_event(computed)
+                for p, (f, k0, k1) in enumerate(pieces):
+                    host[f, k0:k1].copy_(nat[f, k0:k1], non_blocking=True)  # D2H: the next step's input
+                    down_done[p].record(down_stream)
+                e_host.copy_(energy_dev, non_blocking=True)
+            energy_dev.record_stream(down_stream)
 
-        e2e_step()  # warm-up (allocations, first launches)
+        e2e_begin.record(stream)
+        e2e_step(True)  # warm-up (allocations, first launches)
         torch.cuda.synchronize()
         host.copy_(torch.from_numpy(np.ascontiguousarray(u0_host)).to(e2e_dtype))
         barrier()
         torch.cuda.synchronize()
         e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_start.record(stream)
-        for _ in range(e2e_steps):
-            e2e_step()
+        e2e_begin.record(stream)
+        for i in range(e2e_steps):
+            e2e_step(i == 0)
+        if not args.e2e_serial:
+            stream.wait_stream(down_stream)                              # the last download is in the region
         e_stop.record(stream)
         torch.cuda.synchronize()
         barrier()
         e_ms = max_over_ranks(e_start.elapsed_time(e_stop))
         if not math.isfinite(float(e_host.item())):
             raise RuntimeError("non-finite e2e energy")
-        del dev_nat, ue
+        del dev_nat, ue, nat
 
         # ---- the RHS-level drop-in, as the reference's own loop calls it (N=1 only) ----
         # rk4_step(state, t, dt, lambda t, y: op.rhs(y)) on a float64 numpy state: every RHS call
@@ -744,6 +779,10 @@ def run_b200(args) -> None:
         "e2e": {"value": e2e_gflops, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": e2e_steps, "ms_per_step": e_ms / e2e_steps,
                 "host_dtype": str(e2e_dtype).replace("torch.", ""),
+                "overlap": "none (--e2e-serial)" if args.e2e_serial else (
+                    "%d contiguous pieces: the upload of piece p for step i+1 waits for the download of "
+                    "piece p from step i; the pack waits for every upload (download of step i overlaps "
+                    "upload of step i+1, full-duplex PCIe)" % len(pieces)),
                 "path": "dependent chain through the public API, per step: pinned natural host state H2D -> "
                         "op.to_padded -> op.advance(1 LSRK4 step) -> op.from_padded -> D2H into the same "
                         "host buffer (the next step's input) + energy scalar D2H"},
@@ -782,6 +821,9 @@ def main(argv=None) -> None:
                     help="extra config rows at N=1: default (%s), all, none, or a comma list of %s"
                          % (",".join(DEFAULT_EXTRAS), ",".join(EXTRAS)))
     ap.add_argument("--e2e-steps", type=int, default=None, help="e2e steps (default: --steps)")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="e2e copy pieces per field slab")
+    ap.add_argument("--e2e-serial", action="store_true",
+                    help="e2e copies as one H2D and one D2H per step, nothing overlapped")
     ap.add_argument("--dropin-steps", type=int, default=1,
                     help="steps of the RHS-level drop-in leg (reference call pattern, host numpy LSRK; 0: skip)")
     ap.add_argument("--element-order", choices=("auto", "natural", "morton", "columns", "greedy"), default="auto",

@@ -506,6 +506,7 @@ def run_b200(args) -> None:
     from paper_0901_1024_b200 import (CavityMode, build_b200_operator, build_reference_element, compute_geometry,
                                       generate_box_mesh, map_nodes, stable_dt)
     from paper_0901_1024_b200.perfmodel import bytes_per_element_stage, dofs, flops_per_element_stage
+    from paper_0901_1024_b200.hoststep import HostStepper
 
     world, rank, local = _dist_env()
     # DGM_BENCH_ONE_GPU=1 (testing only): every rank on device 0, to exercise the N > 1 path on a
@@ -617,77 +618,39 @@ def run_b200(args) -> None:
 
         # ---- end to end through the public API with host buffers (a dependent chain) ----
         # The reference user's state lives on the host in float64 (natural (6, K, Np) layout).  Every
-        # e2e step uploads the current host state (pinned), packs it, runs one LSRK4 step, unpacks,
-        # downloads the new state into the same host buffer -- the next step's input -- plus the
-        # energy scalar.  The copies move contiguous pieces (--e2e-chunks per field slab) on their own
-        # streams: the upload of piece p for step i+1 waits for the download of piece p from step i,
-        # and the step's pack waits for all six uploads, so every step still computes on the previous
-        # step's downloaded output; what overlaps is the download of step i with the upload of step i+1
-        # (PCIe is full duplex).  --e2e-serial: one copy per direction, nothing overlapped.
+        # e2e step is one HostStepper.step call (paper_0901_1024_b200/hoststep.py): upload the current
+        # host state (pinned), pack, one LSRK4 step, unpack, download the new state into the same host
+        # buffer -- the next step's input -- plus the energy scalar.  The upload of piece p for step i+1
+        # waits for the download of piece p from step i and the pack waits for every upload, so every
+        # step computes on the previous step's downloaded output; what overlaps is the download of step
+        # i with the upload of step i+1 (PCIe is full duplex).  --e2e-serial: one copy per direction.
         e2e_steps = max(1, args.steps if args.e2e_steps is None else min(args.steps, args.e2e_steps))
         e2e_dtype = {"f32": torch.float32, "f64": torch.float64}[args.e2e_dtype]
         host = torch.from_numpy(np.ascontiguousarray(u0_host)).to(e2e_dtype).pin_memory()
-        e_host = torch.empty(1, dtype=torch.float64).pin_memory()
-        dev_nat = torch.empty(host.shape, dtype=e2e_dtype, device=dev)
-        nat = torch.empty(host.shape, dtype=e2e_dtype, device=dev)
-        ue = op.empty_state()
+        e_host = torch.zeros(1, dtype=torch.float64).pin_memory()
         h2d = host.numel() * host.element_size()
         d2h = h2d + 8
-        up_stream, down_stream = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        kb = [round(j * op.num_elements / args.e2e_chunks) for j in range(args.e2e_chunks + 1)]
-        pieces = [(f, kb[j], kb[j + 1]) for f in range(N_FIELDS_E2E) for j in range(args.e2e_chunks)]
-        down_done = [torch.cuda.Event() for _ in pieces]
-        up_done, computed, e2e_begin = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
-
-        def e2e_step(first: bool):
-            if args.e2e_serial:
-                dev_nat.copy_(host, non_blocking=True)                   # H2D of this step's input
-            else:
-                with torch.cuda.stream(up_stream):
-                    up_stream.wait_event(e2e_begin)
-                    for p, (f, k0, k1) in enumerate(pieces):
-                        if not first:
-                            up_stream.wait_event(down_done[p])           # step i's piece p has landed
-                        dev_nat[f, k0:k1].copy_(host[f, k0:k1], non_blocking=True)  # H2D of this step's input
-                    up_done.record(up_stream)
-                stream.wait_event(up_done)
-            op.to_padded(dev_nat, out=ue)                                # pack (natural -> padded, cast)
-            advance(ue, 1)                                               # 5 fused stage launches
-            op.from_padded(ue, e2e_dtype, out=nat)                       # unpack
-            energy_dev = op.mass_norm(ue, 1.0, 1.0)                      # per-step energy scalar
-            if args.e2e_serial:
-                host.copy_(nat, non_blocking=True)                       # D2H: the next step's input
-                e_host.copy_(energy_dev, non_blocking=True)
-                return
-            computed.record(stream)
-            with torch.cuda.stream(down_stream):
-                down_stream.wait_event(computed)
-                for p, (f, k0, k1) in enumerate(pieces):
-                    host[f, k0:k1].copy_(nat[f, k0:k1], non_blocking=True)  # D2H: the next step's input
-                    down_done[p].record(down_stream)
-                e_host.copy_(energy_dev, non_blocking=True)
-            energy_dev.record_stream(down_stream)
-
-        e2e_begin.record(stream)
-        e2e_step(True)  # warm-up (allocations, first launches)
+        stepper = HostStepper(op, advance=lambda x, dt_, n: advance(x, n), chunks=args.e2e_chunks,
+                              serial=args.e2e_serial)
+        stepper.step(host, dt, 1, energy_out=e_host)  # warm-up (allocations, first launches)
+        stepper.join()
         torch.cuda.synchronize()
         host.copy_(torch.from_numpy(np.ascontiguousarray(u0_host)).to(e2e_dtype))
         barrier()
         torch.cuda.synchronize()
         e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_start.record(stream)
-        e2e_begin.record(stream)
-        for i in range(e2e_steps):
-            e2e_step(i == 0)
-        if not args.e2e_serial:
-            stream.wait_stream(down_stream)                              # the last download is in the region
+        for _ in range(e2e_steps):  # one public-API call per step, as a user's loop would make them
+            stepper.step(host, dt, 1, energy_out=e_host)
+        stepper.join()  # the last download is inside the timed region
         e_stop.record(stream)
         torch.cuda.synchronize()
         barrier()
         e_ms = max_over_ranks(e_start.elapsed_time(e_stop))
         if not math.isfinite(float(e_host.item())):
             raise RuntimeError("non-finite e2e energy")
-        del dev_nat, ue, nat
+        pieces = len(stepper._buffers(e2e_dtype)["pieces"])
+        del stepper
 
         # ---- the RHS-level drop-in, as the reference's own loop calls it (N=1 only) ----
         # rk4_step(state, t, dt, lambda t, y: op.rhs(y)) on a float64 numpy state: every RHS call
@@ -782,10 +745,10 @@ def run_b200(args) -> None:
                 "overlap": "none (--e2e-serial)" if args.e2e_serial else (
                     "%d contiguous pieces: the upload of piece p for step i+1 waits for the download of "
                     "piece p from step i; the pack waits for every upload (download of step i overlaps "
-                    "upload of step i+1, full-duplex PCIe)" % len(pieces)),
-                "path": "dependent chain through the public API, per step: pinned natural host state H2D -> "
-                        "op.to_padded -> op.advance(1 LSRK4 step) -> op.from_padded -> D2H into the same "
-                        "host buffer (the next step's input) + energy scalar D2H"},
+                    "upload of step i+1, full-duplex PCIe)" % pieces),
+                "path": "dependent chain through the public API, one HostStepper.step per step: pinned natural "
+                        "host state H2D -> op.to_padded -> advance(1 LSRK4 step) -> op.from_padded -> D2H "
+                        "into the same host buffer (the next step's input) + energy scalar D2H"},
         "gpu_launches": launches,
         "clocks": clk,
         "energy_after": energy,

@@ -27,6 +27,10 @@ def __getattr__(name):
         from . import driver
 
         return getattr(driver, name)
+    if name == "HostStepper":
+        from . import hoststep
+
+        return hoststep.HostStepper
     if name in ("build_face_maps", "FaceMaps"):
         from . import facemaps
 
@@ -41,5 +45,5 @@ __all__ = [
     "map_nodes", "read_tetgen", "FACE_AREAS", "FACE_UNIT_NORMALS", "FACE_VERTEX_IDS", "NUM_FACES",
     "REFERENCE_VERTICES", "ReferenceElement", "build_reference_element", "face_node_permutation",
     "simplex_node_count", "RK_A", "RK_B", "RK_C", "rk4_step", "B200MaxwellOperator", "build_b200_operator",
-    "build_face_maps", "FaceMaps", "run_cavity", "CavityRun", "UnstableRunError",
+    "build_face_maps", "FaceMaps", "run_cavity", "CavityRun", "UnstableRunError", "HostStepper",
 ]

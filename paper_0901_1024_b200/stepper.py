@@ -64,7 +64,18 @@ def rk4_step(state, t: float, dt: float, rhs_fn):
         return y
     y = np.array(state, dtype=np.float64, copy=True)
     res = np.zeros_like(y)
+    tmp = np.empty_like(y)
     for a, b, c in zip(RK_A, RK_B, RK_C):
-        res = a * res + dt * np.asarray(rhs_fn(t + c * dt, y))
-        y = y + b * res
+        k = np.asarray(rhs_fn(t + c * dt, y))
+        if k.dtype != np.float64 or k.shape != y.shape:  # the reference's expressions, verbatim semantics
+            res = a * res + dt * k
+            y = y + b * res
+            continue
+        # the same roundings in place (fl(fl(a res) + fl(dt k)), fl(y + fl(b res))): no 6 K Np temporaries
+        # per stage -- the state passed to rhs_fn is updated in place after it returns
+        np.multiply(k, dt, out=tmp)
+        np.multiply(res, a, out=res)
+        res += tmp
+        np.multiply(res, b, out=tmp)
+        y += tmp
     return y

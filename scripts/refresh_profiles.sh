@@ -18,6 +18,6 @@ if [ -f $S/bench.json ]; then
 fi
 if [ -f $T/pytest_gpu.log ]; then
   cp $T/pytest_gpu.log profiles/r02/pytest_gpu_r2.log
-  for t in memcheck synccheck racecheck; do cp $T/sanitize_$t.log profiles/r02/sanitize/; done
+  for t in memcheck synccheck racecheck; do [ -f $T/sanitize_$t.log ] && cp $T/sanitize_$t.log profiles/r02/sanitize/; done
 fi
 git status --short profiles

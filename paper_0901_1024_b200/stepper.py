@@ -72,10 +72,31 @@ def rk4_step(state, t: float, dt: float, rhs_fn):
             y = y + b * res
             continue
         # the same roundings in place (fl(fl(a res) + fl(dt k)), fl(y + fl(b res))): no 6 K Np temporaries
-        # per stage -- the state passed to rhs_fn is updated in place after it returns
+        # per stage -- the state passed to rhs_fn is updated in place after it returns.  Large states go
+        # through torch's CPU kernels on zero-copy views (all host cores; elementwise, so the same bits).
+        if y.size >= _THREADED_MIN and _torch_cpu() is not None:
+            th = _torch_cpu()
+            ty, tr, tt, tk = th.from_numpy(y), th.from_numpy(res), th.from_numpy(tmp), th.from_numpy(np.ascontiguousarray(k))
+            th.mul(tk, dt, out=tt)
+            tr.mul_(a)
+            tr.add_(tt)
+            th.mul(tr, b, out=tt)
+            ty.add_(tt)
+            continue
         np.multiply(k, dt, out=tmp)
         np.multiply(res, a, out=res)
         res += tmp
         np.multiply(res, b, out=tmp)
         y += tmp
     return y
+
+
+_THREADED_MIN = 1 << 22  # elements (32 MB of float64) from which the stage update runs multi-threaded
+
+
+def _torch_cpu():
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return None
+    return torch

@@ -36,3 +36,18 @@ def test_rk4_step_float32_rhs_keeps_reference_promotion():
         return (0.5 * y).astype(np.float32)
 
     assert np.array_equal(rk4_step(y0, 0.0, 0.02, fn), _reference_form(y0, 0.0, 0.02, fn))
+
+
+def test_rk4_step_threaded_path_bitwise(monkeypatch):
+    """Large states take torch's multi-threaded CPU kernels: still the reference's bits."""
+    import paper_0901_1024_b200.stepper as st
+
+    monkeypatch.setattr(st, "_THREADED_MIN", 1)
+    rng = np.random.default_rng(9)
+    y0 = rng.normal(size=(6, 300, 35))
+    m = rng.normal(size=(35, 35))
+
+    def fn(t, y):
+        return 0.05 * (y @ m) - 0.3 * np.cos(t) * y
+
+    assert np.array_equal(st.rk4_step(y0, 0.1, 0.003, fn), _reference_form(y0, 0.1, 0.003, fn))

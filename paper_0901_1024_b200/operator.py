@@ -272,6 +272,7 @@ class B200MaxwellOperator:
         self._norm_out = torch.zeros(1, dtype=torch.float64, device=self.device)
         n_part = int(lib.dgm_mass_norm_partials(handle, self.num_elements))
         self._partials = torch.zeros(max(n_part, 1), dtype=torch.float64, device=self.device)
+        self._pinned_rhs = {}        # rhs() on numpy states: pinned staging buffers per (in, out) dtype
         self.collect_stats = False   # record CUDA-event times of every stage launch
         self._events: list = []
         self._stats: dict = {}
@@ -499,11 +500,40 @@ class B200MaxwellOperator:
         src = np.asarray(state) if is_numpy else state
         out_dtype = torch.float32 if (src.dtype == np.float32 if is_numpy else src.dtype == torch.float32) \
             else torch.float64
+        if is_numpy:
+            return self._rhs_numpy(src, out_dtype)
         u = self.to_padded(src)
         out = self.from_padded(self.rhs_padded(u), out_dtype)
-        if is_numpy:
-            return out.cpu().numpy()
         return out.to(device=state.device)
+
+    def _rhs_numpy(self, src: np.ndarray, out_dtype: torch.dtype) -> np.ndarray:
+        """rhs() for a host numpy state: staged through cached pinned buffers (the host-side copies run on
+        torch's multi-threaded CPU kernels, the PCIe copies at pinned speed); returns a fresh array."""
+        shape = (N_FIELDS, self.num_elements, self.elem.num_nodes)
+        k, n_p = self.num_elements, self.elem.num_nodes
+        if src.size != N_FIELDS * k * n_p:
+            raise ValueError(f"natural state must have 6*K*Np = {N_FIELDS * k * n_p} values "
+                             f"(shape (6, {k}, {n_p})), got shape {tuple(src.shape)}")
+        if src.dtype not in (np.float32, np.float64):
+            src = src.astype(np.float64)
+        src = np.ascontiguousarray(src).reshape(shape)
+        if not src.flags.writeable:
+            src = src.copy()
+        key = (src.dtype.str, out_dtype)
+        bufs = self._pinned_rhs.get(key)
+        if bufs is None:
+            in_dtype = torch.float64 if src.dtype == np.float64 else torch.float32
+            bufs = (torch.empty(shape, dtype=in_dtype, pin_memory=True),
+                    torch.empty(shape, dtype=out_dtype, pin_memory=True))
+            self._pinned_rhs[key] = bufs
+        host_in, host_out = bufs
+        host_in.copy_(torch.from_numpy(src))
+        out = self.from_padded(self.rhs_padded(self.to_padded(host_in)), out_dtype)
+        host_out.copy_(out, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()  # also frees host_in for the next call
+        result = torch.empty(shape, dtype=out_dtype)
+        result.copy_(host_out)
+        return result.numpy()
 
     def face_states(self, state):
         """(u_minus, u_plus, normals) per face node, boundary side mirrored (oracle.py:50-58).

@@ -506,6 +506,8 @@ class B200MaxwellOperator:
         out = self.from_padded(self.rhs_padded(u), out_dtype)
         return out.to(device=state.device)
 
+    PINNED_RHS_MAX_BYTES = 8 << 30  # per staging buffer; larger numpy states take the pageable path
+
     def _rhs_numpy(self, src: np.ndarray, out_dtype: torch.dtype) -> np.ndarray:
         """rhs() for a host numpy state: staged through cached pinned buffers (the host-side copies run on
         torch's multi-threaded CPU kernels, the PCIe copies at pinned speed); returns a fresh array."""
@@ -523,9 +525,17 @@ class B200MaxwellOperator:
         bufs = self._pinned_rhs.get(key)
         if bufs is None:
             in_dtype = torch.float64 if src.dtype == np.float64 else torch.float32
-            bufs = (torch.empty(shape, dtype=in_dtype, pin_memory=True),
-                    torch.empty(shape, dtype=out_dtype, pin_memory=True))
+            try:
+                if src.nbytes > self.PINNED_RHS_MAX_BYTES:
+                    raise RuntimeError("state too large for pinned staging")
+                bufs = (torch.empty(shape, dtype=in_dtype, pin_memory=True),
+                        torch.empty(shape, dtype=out_dtype, pin_memory=True))
+            except RuntimeError:  # no pinned memory to spare: the pageable path, same results
+                bufs = False
             self._pinned_rhs[key] = bufs
+        if bufs is False:
+            out = self.from_padded(self.rhs_padded(self.to_padded(src)), out_dtype)
+            return out.cpu().numpy()
         host_in, host_out = bufs
         host_in.copy_(torch.from_numpy(src))
         out = self.from_padded(self.rhs_padded(self.to_padded(host_in)), out_dtype)

@@ -170,3 +170,27 @@ def test_host_stepper_matches_device_stepping(serial):
     assert energy.item() > 0
     with pytest.raises(ValueError):
         st.step(host[:, :1], dt)
+
+
+@pytest.mark.gpu
+def test_rhs_numpy_pageable_fallback_matches_pinned(monkeypatch):
+    """rhs(numpy) through pinned staging and through the pageable fallback give the same array."""
+    import torch
+
+    from paper_0901_1024_b200.operator import B200MaxwellOperator
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    mesh = generate_box_mesh((1.0, 1.0, 1.0), (3, 3, 2))
+    elem = build_reference_element(3)
+    u0 = np.random.default_rng(3).normal(size=(6, mesh.num_elements, elem.num_nodes))
+    op = build_b200_operator(mesh, elem, dtype=torch.float64, device="cuda:0")
+    pinned = op.rhs(u0)
+    again = op.rhs(u0)  # cached buffers reused
+    monkeypatch.setattr(B200MaxwellOperator, "PINNED_RHS_MAX_BYTES", 0)
+    op2 = build_b200_operator(mesh, elem, dtype=torch.float64, device="cuda:0")
+    pageable = op2.rhs(u0)
+    assert pinned.dtype == np.float64 and pinned.shape == u0.shape
+    np.testing.assert_array_equal(pinned, again)
+    np.testing.assert_array_equal(pinned, pageable)
+    assert op2._pinned_rhs[(u0.dtype.str, torch.float64)] is False

@@ -49,7 +49,7 @@ class HostStepper:
                      nat=torch.empty(shape, dtype=dtype, device=op.device), padded=op.empty_state(),
                      up=torch.cuda.Stream(op.device), down=torch.cuda.Stream(op.device), pieces=pieces,
                      down_done=[torch.cuda.Event() for _ in pieces], up_done=torch.cuda.Event(),
-                     computed=torch.cuda.Event(), begin=torch.cuda.Event())
+                     computed=torch.cuda.Event(), energy_done=torch.cuda.Event(), begin=torch.cuda.Event())
             self._bufs[dtype] = b
         return b
 
@@ -85,19 +85,24 @@ class HostStepper:
             op.to_padded(b["dev_nat"], out=b["padded"])
             self._advance(b["padded"], dt, 1)
             op.from_padded(b["padded"], host.dtype, out=b["nat"])
-            energy = op.mass_norm(b["padded"], 1.0, 1.0) if energy_out is not None else None
             if self.serial:
                 host.copy_(b["nat"], non_blocking=True)
-                if energy is not None:
-                    energy_out[:1].copy_(energy, non_blocking=True)
+                if energy_out is not None:
+                    energy_out[:1].copy_(op.mass_norm(b["padded"], 1.0, 1.0), non_blocking=True)
                 continue
             b["computed"].record(stream)
+            # the energy reduction runs on the compute stream while the downloads drain (it only reads
+            # the padded state, which the next step's pack rewrites after every upload has landed)
+            energy = op.mass_norm(b["padded"], 1.0, 1.0) if energy_out is not None else None
+            if energy is not None:
+                b["energy_done"].record(stream)
             with torch.cuda.stream(b["down"]):
                 b["down"].wait_event(b["computed"])
                 for p, (f, k0, k1) in enumerate(b["pieces"]):
                     host[f, k0:k1].copy_(b["nat"][f, k0:k1], non_blocking=True)
                     b["down_done"][p].record(b["down"])
                 if energy is not None:
+                    b["down"].wait_event(b["energy_done"])
                     energy_out[:1].copy_(energy, non_blocking=True)
             if energy is not None:
                 energy.record_stream(b["down"])

@@ -616,7 +616,9 @@ int dgm_pack(int32_t order, int32_t dtype, const void* natural, int32_t natural_
     using C = dgm::Cfg<N, T>;
     return natural_dispatch(natural_dtype, [&](auto tn) -> int {
       using TN = decltype(tn);
-      dgm::pack_kernel<N, T, TN><<<grid_for(6 * num_elements * C::NPG, 256), 256, 0,
+      // y = field; the six fields share the usual block cap (grid-stride loop)
+      const dim3 grid((unsigned)grid_for((num_elements * (C::NPG / C::VEC) + 5) / 6, 256), 6);
+      dgm::pack_kernel<N, T, TN><<<grid, 256, 0,
                                    static_cast<cudaStream_t>(stream)>>>(
           static_cast<const TN*>(natural), perm, static_cast<T*>(padded), num_elements, field_stride);
       return cuda_check(cudaGetLastError(), "pack_kernel launch");
@@ -635,7 +637,8 @@ int dgm_unpack(int32_t order, int32_t dtype, const void* padded, const int64_t* 
     using C = dgm::Cfg<N, T>;
     return natural_dispatch(natural_dtype, [&](auto tn) -> int {
       using TN = decltype(tn);
-      dgm::unpack_kernel<N, T, TN><<<grid_for(6 * num_elements * C::NP, 256), 256, 0,
+      const dim3 grid((unsigned)grid_for((num_elements * C::NP + 5) / 6, 256), 6);
+      dgm::unpack_kernel<N, T, TN><<<grid, 256, 0,
                                      static_cast<cudaStream_t>(stream)>>>(
           static_cast<const T*>(padded), perm, static_cast<TN*>(natural), num_elements, field_stride);
       return cuda_check(cudaGetLastError(), "unpack_kernel launch");

@@ -91,10 +91,10 @@ struct TcCfg {
   static constexpr int KV = (3 * NPK + 7) / 8 * 8; // volume part of K, padded to a K step
   static constexpr int KT = KV + 4 * NFPK;
   static constexpr int KS = KT / 8;                // K steps (one kind::tf32 MMA each)
-  // Lane mapping.  MAP 0 (N <= 6): 64 elements per CTA, M-tile t = [E_t of the 64 elements |
+  // Lane mapping.  MAP 0 (N <= 4, 6): 64 elements per CTA, M-tile t = [E_t of the 64 elements |
   // H_t of the 64 elements].  MAP 1 (N = 7, 8, where a 64-element u tile no longer fits in smem),
   // M-tiles component-major: N=8, 32 elements per CTA, tile 0 = [E_x | E_y | E_z | H_x], tile 1 =
-  // [H_y | H_z | pad | pad] (32 lanes per component); N=7, 42 elements, tile 0 = [E_x | E_y | E_z],
+  // [H_y | H_z | pad | pad] (32 lanes per component); N=5, 7, 42 elements, tile 0 = [E_x | E_y | E_z],
   // tile 1 = [H_x | H_y | H_z] (42 lanes per component, 2 pad lanes).
   // MAP 2 (N = 9): TE = 21 elements per CTA, one M-tile holding all six components, lane = TE c + e
   // (126 of 128 lanes used).
@@ -105,7 +105,15 @@ struct TcCfg {
 #else
   static constexpr bool SMALL = false;
 #endif
-  static constexpr int MAP = SMALL ? 2 : (N <= 6 ? 0 : (N <= 8 ? 1 : 2));
+  // N=5 on the 42-element three-component MAP 1 tiles at two CTAs per SM (TMEM 128 + 4 x 32 columns,
+  // 107 KB smem, role-based registers) instead of one 64-element MAP 0 CTA: C2 N=5 168.5 -> 139.1 us
+  // per stage, -12 % at 547k tets (profiles/r02/ab_n5_map1.txt); -DDGM_TC_N5_MAP0 restores MAP 0
+#ifdef DGM_TC_N5_MAP0
+  static constexpr bool N5M1 = false;
+#else
+  static constexpr bool N5M1 = N == 5 && !SMALL;
+#endif
+  static constexpr int MAP = SMALL ? 2 : (N5M1 ? 1 : (N <= 6 ? 0 : (N <= 8 ? 1 : 2)));
 #ifdef DGM_TC_INLINE_FLUX
   // experiment: each producer computes its own face values inside the K-loop (no flux passes)
   static constexpr bool INLINE_FLUX = MAP == 0;
@@ -123,9 +131,9 @@ struct TcCfg {
   // 192: C2 N=7 439 -> 384 us per stage, profiles/r02/ab_map1_te42.txt); N=8 has no shared memory for
   // more than 32.  DGM_TC_TE7 overrides it for experiments
 #ifdef DGM_TC_TE7
-  static constexpr int TE_MAP1 = N == 7 ? DGM_TC_TE7 : 32;
+  static constexpr int TE_MAP1 = (N == 7 || N5M1) ? DGM_TC_TE7 : 32;
 #else
-  static constexpr int TE_MAP1 = N == 7 ? 42 : 32;
+  static constexpr int TE_MAP1 = (N == 7 || N5M1) ? 42 : 32;
 #endif
   // MAP 1 with TE != 32: three components per M-tile (tile t = components 3t..3t+2, lane = TE c' + e)
   static constexpr bool M1C3 = MAP == 1 && TE_MAP1 != 32;
@@ -160,7 +168,7 @@ struct TcCfg {
 #ifdef DGM_TC_NO_RREG
   static constexpr bool RREG = false;
 #else
-  static constexpr bool RREG = !SMALL && !MERGE && N <= 4 && PWARPS == 8;
+  static constexpr bool RREG = !SMALL && !MERGE && (N <= 4 || N5M1) && PWARPS == 8;
 #endif
   static constexpr int REG_AUX = 32, REG_PROD = 104;
   // flux pass: u+ of in-tile and out-of-tile neighbours through one generic-address load path
@@ -183,7 +191,7 @@ struct TcCfg {
   static constexpr int ACC_COLS = MT * NB;
   static constexpr int A_COL0 = (ACC_COLS + 31) / 32 * 32;
   static constexpr int A_STAGE_COLS = MT * 16;     // M-tiles x (8 hi + 8 lo)
-  static constexpr int CTAS = SMALL ? 3 : (N <= 4 ? 2 : 1);  // CTAs per SM (TMEM and smem split between them)
+  static constexpr int CTAS = SMALL ? 3 : ((N <= 4 || N5M1) ? 2 : 1);  // CTAs per SM (TMEM and smem split between them)
   static constexpr int TMEM_COLS = CTAS == 3 ? 128 : 512 / CTAS;  // power of two
   static constexpr int AST0 = (TMEM_COLS - A_COL0) / A_STAGE_COLS;
   static constexpr int AST = AST0 > 6 ? 6 : AST0;   // A ring stages in TMEM
@@ -237,7 +245,7 @@ struct TcCfg {
   static constexpr int SROW = TE + srow_pad();
 #endif
   static constexpr int B_STEP_BYTES = 2 * 2 * NB * 16;   // hi/lo x 2 chunks x NB rows x 16 B
-  static constexpr int NBS = N <= 5 ? 6 : 4;       // B ring slots (a slot is refilled when its MMAs complete)
+  static constexpr int NBS = (N <= 5 && !N5M1) ? 6 : 4;       // B ring slots (a slot is refilled when its MMAs complete)
   static constexpr uint32_t ROWS_BYTES = TE * NPG * 4;   // one field slab of the tile
   // shared-memory carve-up (bytes)
   static constexpr size_t OFF_U = 0;

@@ -22,7 +22,8 @@ def main():
     bw = d["roofline"]["peak"]
     rows = {"C1": ("C1 N=3, 1,512 tets, 100 steps, CUDA graph", "SIMT f32, few-tile variant", "c1")}
     for n in range(1, 10):
-        kern = "SIMT f32" if n <= 2 else "tensor v1" + {7: " (42-el. tiles)", 9: " (21-el. tiles)"}.get(n, "")
+        kern = "SIMT f32" if n <= 2 else "tensor v1" + {5: " (42-el. tiles, 2 CTAs/SM)", 7: " (42-el. tiles)",
+                                                          9: " (21-el. tiles)"}.get(n, "")
         rows["C2_N%d" % n] = ("C2 N=%d, 48k" % n, kern, "c2n%d" % n)
     rows["C3_f64"] = ("C3 N=4, 998,250, fp64", "SIMT + DMMA", "c3f64")
     rows["C4"] = ("C4 N=4, 7,986,000, 1 GPU", "tensor v1", "c4")

@@ -1,7 +1,8 @@
 """Loose performance guards (a regression of several x fails; the numbers themselves live in bench.py).
 
-C1 through the CUDA-graph path (launch-bound) and the fp64 kernel at 48k tets; bounds
-are ~3x the round-2 measurements (C1 14.7 us, fp64 N=4 at 48k ~0.2 ms per stage).
+C1 through the CUDA-graph path (launch-bound), the fp64 kernel and the tensor kernels'
+lane mappings at 48k tets; bounds are ~3x the round-2 measurements (C1 6.9-7.7 us, fp64
+N=4 at 48k 0.2 ms per stage).
 """
 
 import pytest
@@ -48,3 +49,14 @@ def test_fp64_stage_time():
     us = _us_per_stage((20, 20, 20), 4, torch.float64, 10, False)
     print(f"fp64 N=4 48k {us:.1f} us per stage")
     assert us < 700.0
+
+
+@pytest.mark.parametrize("order,bound_us", [(4, 250.0), (5, 420.0), (7, 1150.0), (9, 2450.0)])
+def test_tensor_stage_time(order, bound_us):
+    """The tensor kernels per lane mapping (N=4 MAP 0 two CTAs/SM, N=5 / 7 the 42-element three-component
+    tiles, N=9 the 21-element tile) at 48k tets: ~3x the round-2 stage times (79 / 139 / 384 / 818 us)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    us = _us_per_stage((20, 20, 20), order, torch.float32, 6, False)
+    print(f"tensor N={order} 48k {us:.1f} us per stage")
+    assert us < bound_us
